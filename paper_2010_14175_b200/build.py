@@ -1,0 +1,78 @@
+"""Build libafsai_b200.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
+
+Each .cu under csrc/ is compiled separately (setup_kernel.cu with -fmad=false so
+the only fused multiply-adds are the explicit fma() of the arithmetic contract,
+DESIGN.md §3.1), then linked with NCCL into lib/libafsai_b200.so.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "lib")
+OBJDIR = os.path.join(HERE, "build_obj")
+LIB = os.path.join(LIBDIR, "libafsai_b200.so")
+ROOT = os.path.dirname(HERE)
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dirs():
+    try:
+        import nvidia.nccl as nc  # the NCCL torch loads
+        base = list(nc.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def _flags_for(src: str):
+    flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+             "-Xptxas", "-v"] + ARCH
+    if os.path.basename(src) == "setup_kernel.cu":
+        flags += ["-fmad=false"]
+    return flags
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
+    inc, libdir = _nccl_dirs()
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "afsai.h")]
+    newest_hdr = max(os.path.getmtime(h) for h in hdrs)
+    objs = []
+    for s in srcs:
+        o = os.path.join(OBJDIR, os.path.basename(s) + ".o")
+        objs.append(o)
+        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
+            cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s)
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {s}")
+            log = os.path.join(OBJDIR, os.path.basename(s) + ".ptxas.txt")
+            with open(log, "w") as f:
+                f.write(r.stderr)
+            if verbose:
+                sys.stderr.write(r.stderr)
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + [
+            "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}", "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("link failed")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

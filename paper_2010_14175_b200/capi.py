@@ -1,0 +1,256 @@
+"""Thin ctypes binding of include/afsai.h (argument marshalling only).
+
+Every function here forwards to libafsai_b200.so under the same name; all
+computation happens in the library's CUDA kernels.  There is no fallback: if
+the shared library is missing or fails to load, importing this module raises.
+Tensors may live on the GPU or on the host (the library stages host arrays).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libafsai_b200.so")
+
+AFSAI_OK, AFSAI_EINVAL, AFSAI_ENOTSPD, AFSAI_ECUDA, AFSAI_ENCCL, AFSAI_ENOMEM, AFSAI_ENOTCONV, AFSAI_ELIMIT = range(8)
+STOP_NAMES = {0: "kmax", 1: "cap", 2: "no_candidates", 3: "tolerance"}
+
+# every symbol declared in include/afsai.h
+EXPORTS = [
+    "afsai_version", "afsai_strerror", "afsai_ctx_create", "afsai_nccl_unique_id", "afsai_ctx_create_nccl",
+    "afsai_ctx_rank", "afsai_ctx_destroy", "afsai_setup", "afsai_apply", "afsai_pcg", "afsai_factor_nnz",
+    "afsai_factor_copy", "afsai_factor_trace", "afsai_factor_stats", "afsai_factor_destroy",
+    "afsai_ctx_launches", "afsai_probe_dfma_peak", "afsai_ctx_set_timing", "afsai_ctx_kernel_times",
+]
+KERNEL_CLASSES = ["setup_rows", "assemble", "transpose", "spmv_G", "spmv_Gt", "spmv_A", "vector", "comm"]
+
+
+class afsai_csr_t(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row_begin", ctypes.c_int64), ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("val", ctypes.c_void_p)]
+
+
+class afsai_params_t(ctypes.Structure):
+    _fields_ = [("nsteps", ctypes.c_int32), ("s", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("max_row_nnz", ctypes.c_int32)]
+
+
+class afsai_status_t(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("row", ctypes.c_int64), ("step", ctypes.c_int32),
+                ("msg", ctypes.c_char * 160)]
+
+
+class afsai_setup_stats_t(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("nnz_G", ctypes.c_int64), ("nnz_Gt", ctypes.c_int64),
+                ("rows_by_reason", ctypes.c_int64 * 4), ("steps_total", ctypes.c_int64),
+                ("fma_border", ctypes.c_int64), ("fma_backsub", ctypes.c_int64), ("fma_grad", ctypes.c_int64),
+                ("grad_entries", ctypes.c_int64), ("ms_total", ctypes.c_double), ("ms_rows", ctypes.c_double),
+                ("ms_assemble", ctypes.c_double), ("ms_transpose", ctypes.c_double), ("ms_halo", ctypes.c_double),
+                ("table_size", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32), ("retried_rows", ctypes.c_int32),
+                ("halo_rows", ctypes.c_int32)]
+
+    def to_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            d[name] = list(v) if name == "rows_by_reason" else v
+        return d
+
+
+class afsai_pcg_report_t(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32), ("rel_res", ctypes.c_double),
+                ("true_rel_res", ctypes.c_double), ("ms_solve", ctypes.c_double), ("ms_per_iter", ctypes.c_double)]
+
+    def to_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+def load_library(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"libafsai_b200.so not built ({path}); run __graft_entry__.build()")
+    lib = ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+    P, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    sig = {
+        "afsai_version": ([], ctypes.c_char_p),
+        "afsai_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "afsai_ctx_create": ([P, P], ctypes.c_int),
+        "afsai_nccl_unique_id": ([P], ctypes.c_int),
+        "afsai_ctx_create_nccl": ([P, P, P, i32, i32], ctypes.c_int),
+        "afsai_ctx_rank": ([P, P, P], ctypes.c_int),
+        "afsai_ctx_destroy": ([P], None),
+        "afsai_setup": ([P, ctypes.POINTER(afsai_csr_t), ctypes.POINTER(afsai_params_t), P,
+                         ctypes.POINTER(afsai_status_t)], ctypes.c_int),
+        "afsai_apply": ([P, P, P, P], ctypes.c_int),
+        "afsai_pcg": ([P, ctypes.POINTER(afsai_csr_t), P, P, P, f64, i32, ctypes.POINTER(afsai_pcg_report_t),
+                       ctypes.POINTER(afsai_status_t)], ctypes.c_int),
+        "afsai_factor_nnz": ([P, P, P], ctypes.c_int),
+        "afsai_factor_copy": ([P, i32, P, P, P], ctypes.c_int),
+        "afsai_factor_trace": ([P, P, P], ctypes.c_int),
+        "afsai_factor_stats": ([P, ctypes.POINTER(afsai_setup_stats_t)], ctypes.c_int),
+        "afsai_factor_destroy": ([P], None),
+        "afsai_ctx_launches": ([P], i64),
+        "afsai_probe_dfma_peak": ([P, P, P], ctypes.c_int),
+        "afsai_ctx_set_timing": ([P, i32], ctypes.c_int),
+        "afsai_ctx_kernel_times": ([P, P, P], ctypes.c_int),
+    }
+    for name in EXPORTS:
+        fn = getattr(lib, name)  # AttributeError if the symbol is missing
+        fn.argtypes, fn.restype = sig[name]
+    return lib
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+class AfsaiError(RuntimeError):
+    def __init__(self, code, status: afsai_status_t | None = None, where: str = ""):
+        msg = lib().afsai_strerror(code).decode()
+        self.code = code
+        self.row = status.row if status is not None else -1
+        self.step = status.step if status is not None else -1
+        detail = status.msg.decode(errors="replace") if status is not None else ""
+        super().__init__(f"{where}: {msg} (code {code}) {detail} row={self.row} step={self.step}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return ctypes.c_void_p(t.data_ptr())
+    return t.ctypes.data_as(ctypes.c_void_p)  # numpy
+
+
+def make_csr(rowptr, col, val, n_cols: int, row_begin: int = 0) -> afsai_csr_t:
+    n_rows = (rowptr.numel() if hasattr(rowptr, "numel") else len(rowptr)) - 1
+    nnz = int(col.numel() if hasattr(col, "numel") else len(col))
+    c = afsai_csr_t(n_rows, n_cols, nnz, row_begin, None, None, None)
+    c.rowptr = _ptr(rowptr).value if n_rows >= 0 else None
+    c.col = _ptr(col).value
+    c.val = _ptr(val).value
+    return c
+
+
+# ----------------------------------------------------------------- same-name wrappers
+def afsai_ctx_create(stream_ptr: int = 0):
+    h = ctypes.c_void_p()
+    rc = lib().afsai_ctx_create(ctypes.byref(h), ctypes.c_void_p(stream_ptr))
+    if rc:
+        raise AfsaiError(rc, where="afsai_ctx_create")
+    return h
+
+
+def afsai_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().afsai_nccl_unique_id(buf)
+    if rc:
+        raise AfsaiError(rc, where="afsai_nccl_unique_id")
+    return buf.raw
+
+
+def afsai_ctx_create_nccl(stream_ptr: int, uid: bytes, rank: int, nranks: int):
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    rc = lib().afsai_ctx_create_nccl(ctypes.byref(h), ctypes.c_void_p(stream_ptr), buf, rank, nranks)
+    if rc:
+        raise AfsaiError(rc, where="afsai_ctx_create_nccl")
+    return h
+
+
+def afsai_ctx_destroy(ctx):
+    lib().afsai_ctx_destroy(ctx)
+
+
+def afsai_ctx_launches(ctx) -> int:
+    return int(lib().afsai_ctx_launches(ctx))
+
+
+def afsai_setup(ctx, A: afsai_csr_t, nsteps: int, s: int, eps: float, max_row_nnz: int):
+    p = afsai_params_t(nsteps, s, eps, max_row_nnz)
+    f = ctypes.c_void_p()
+    st = afsai_status_t()
+    rc = lib().afsai_setup(ctx, ctypes.byref(A), ctypes.byref(p), ctypes.byref(f), ctypes.byref(st))
+    if rc:
+        raise AfsaiError(rc, st, "afsai_setup")
+    return f
+
+
+def afsai_apply(ctx, F, r, z):
+    rc = lib().afsai_apply(ctx, F, _ptr(r), _ptr(z))
+    if rc:
+        raise AfsaiError(rc, where="afsai_apply")
+
+
+def afsai_pcg(ctx, A: afsai_csr_t, F, b, x, tol: float = 1e-8, max_iters: int = 10000, raise_notconv=False):
+    rep = afsai_pcg_report_t()
+    st = afsai_status_t()
+    rc = lib().afsai_pcg(ctx, ctypes.byref(A), F, _ptr(b), _ptr(x), float(tol), int(max_iters),
+                         ctypes.byref(rep), ctypes.byref(st))
+    if rc and (rc != AFSAI_ENOTCONV or raise_notconv):
+        raise AfsaiError(rc, st, "afsai_pcg")
+    return rep
+
+
+def afsai_factor_nnz(F):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib().afsai_factor_nnz(F, ctypes.byref(a), ctypes.byref(b))
+    if rc:
+        raise AfsaiError(rc, where="afsai_factor_nnz")
+    return a.value, b.value
+
+
+def afsai_factor_copy(F, which: int, rowptr, col, val):
+    rc = lib().afsai_factor_copy(F, which, _ptr(rowptr), _ptr(col), _ptr(val))
+    if rc:
+        raise AfsaiError(rc, where="afsai_factor_copy")
+
+
+def afsai_factor_trace(F, steps, reason):
+    rc = lib().afsai_factor_trace(F, _ptr(steps), _ptr(reason))
+    if rc:
+        raise AfsaiError(rc, where="afsai_factor_trace")
+
+
+def afsai_factor_stats(F) -> afsai_setup_stats_t:
+    s = afsai_setup_stats_t()
+    rc = lib().afsai_factor_stats(F, ctypes.byref(s))
+    if rc:
+        raise AfsaiError(rc, where="afsai_factor_stats")
+    return s
+
+
+def afsai_factor_destroy(F):
+    lib().afsai_factor_destroy(F)
+
+
+def afsai_probe_dfma_peak(ctx):
+    fl, ms = ctypes.c_double(), ctypes.c_double()
+    rc = lib().afsai_probe_dfma_peak(ctx, ctypes.byref(fl), ctypes.byref(ms))
+    if rc:
+        raise AfsaiError(rc, where="afsai_probe_dfma_peak")
+    return fl.value, ms.value
+
+
+def afsai_ctx_set_timing(ctx, enable: bool):
+    rc = lib().afsai_ctx_set_timing(ctx, 1 if enable else 0)
+    if rc:
+        raise AfsaiError(rc, where="afsai_ctx_set_timing")
+
+
+def afsai_ctx_kernel_times(ctx) -> dict:
+    """{class: (launches, total_ms)} since the last afsai_ctx_set_timing."""
+    n = len(KERNEL_CLASSES)
+    la = (ctypes.c_int64 * n)()
+    ms = (ctypes.c_double * n)()
+    rc = lib().afsai_ctx_kernel_times(ctx, la, ms)
+    if rc:
+        raise AfsaiError(rc, where="afsai_ctx_kernel_times")
+    return {k: (int(la[i]), float(ms[i])) for i, k in enumerate(KERNEL_CLASSES)}

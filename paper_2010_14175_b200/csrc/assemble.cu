@@ -1,0 +1,250 @@
+// assemble.cu -- input validation, CSR assembly of G (count -> scan -> fill,
+// SURVEY §8(a) a7) and the deterministic transpose G^T (a8).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "afsai_internal.h"
+#include "assemble.h"
+
+namespace afsai {
+
+constexpr unsigned kFullA = 0xffffffffu;
+
+// ---------------------------------------------------------------- validation
+// One warp per row: columns strictly increasing and in [0, n_cols), diagonal
+// present and > 0, values finite.  err gets atomicMin((row << 8) | reason).
+__global__ void validate_rows_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                     int64_t n_rows, int64_t row_begin, int64_t n_cols,
+                                     unsigned long long *err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+        const int64_t e0 = rowptr[r] - base, e1 = rowptr[r + 1] - base;
+        const int64_t gi = r + row_begin;
+        int bad = 0;
+        bool diag = false;
+        if (e1 < e0) bad = 1;
+        for (int64_t e = e0 + lane; e < e1 && !bad; e += 32) {
+            const int32_t c = col[e];
+            const double v = val[e];
+            if (c < 0 || c >= n_cols) bad = 2;
+            else if (e > e0 && col[e - 1] >= c) bad = 3;
+            else if (!isfinite(v)) bad = 4;
+            else if (c == gi) {
+                diag = true;
+                if (!(v > 0.0)) bad = 5;
+            }
+        }
+        bad = __reduce_max_sync(kFullA, bad);
+        const bool has_diag = __any_sync(kFullA, diag);
+        if (!bad && !has_diag) bad = 6;
+        if (bad && lane == 0) atomicMin(err, ((unsigned long long)gi << 8) | (unsigned long long)bad);
+    }
+}
+
+// max row length (sizes the per-row candidate table)
+__global__ void row_len_max_kernel(const int64_t *rowptr, int64_t n_rows, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long l = (unsigned long long)(rowptr[r + 1] - rowptr[r]);
+        m = l > m ? l : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(kFullA, m, o);
+        m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// bitwise symmetry (AFSAI_VALIDATE=1): for each stored (i, j) with row j held
+// locally, (j, i) must exist with identical bits.
+__global__ void symmetry_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                int64_t n_rows, int64_t row_begin, unsigned long long *err) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = tid; r < n_rows; r += nt) {
+        const int64_t gi = r + row_begin;
+        for (int64_t e = rowptr[r] - base; e < rowptr[r + 1] - base; ++e) {
+            const int64_t j = col[e];
+            if (j < row_begin || j >= row_begin + n_rows) continue;
+            int64_t lo = rowptr[j - row_begin] - base, hi = rowptr[j - row_begin + 1] - base;
+            bool ok = false;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (col[mid] < gi) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo < rowptr[j - row_begin + 1] - base && col[lo] == gi)
+                ok = (__double_as_longlong(val[lo]) == __double_as_longlong(val[e]));
+            if (!ok) atomicMin(err, ((unsigned long long)gi << 8) | 7ull);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- exclusive scan
+// int32 counts -> int64 offsets, out[n] = total.  Three passes over tiles of
+// kScanTile elements: tile sums, scan of tile sums (one block), tile scans.
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t *total) {
+    __shared__ int64_t warp_tot[kScanThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(kFullA, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = (lane < kScanThreads / 32) ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(kFullA, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kScanThreads / 32) warp_tot[lane] = w;
+    }
+    __syncthreads();
+    const int64_t before = (wid > 0 ? warp_tot[wid - 1] : 0) + (x - v);
+    *total = warp_tot[kScanThreads / 32 - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void scan_tile_sums(const int32_t *in, int64_t n, int64_t *tile_sums) {
+    const int64_t t0 = (int64_t)blockIdx.x * kScanTile;
+    int64_t s = 0;
+    for (int k = 0; k < kScanItems; ++k) {
+        const int64_t idx = t0 + (int64_t)k * kScanThreads + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    int64_t tot;
+    block_exclusive_scan(s, &tot);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void scan_tile_offsets(int64_t *tile_sums, int64_t ntiles) {
+    // single block, sequential chunks
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < ntiles; c0 += kScanThreads) {
+        const int64_t idx = c0 + threadIdx.x;
+        const int64_t v = idx < ntiles ? tile_sums[idx] : 0;
+        int64_t tot;
+        const int64_t ex = block_exclusive_scan(v, &tot);
+        if (idx < ntiles) tile_sums[idx] = carry + ex;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) tile_sums[ntiles] = carry;
+}
+
+__global__ void scan_tiles(const int32_t *in, int64_t n, const int64_t *tile_off, int64_t *out) {
+    // each thread owns kScanItems consecutive elements
+    const int64_t t0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int32_t v[kScanItems];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (t0 + k < n) ? in[t0 + k] : 0;
+        s += v[k];
+    }
+    int64_t tot;
+    int64_t ex = block_exclusive_scan(s, &tot) + tile_off[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (t0 + k < n) out[t0 + k] = ex;
+        ex += v[k];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_off[gridDim.x];
+}
+
+cudaError_t exclusive_scan(const int32_t *in, int64_t n, int64_t *out, int64_t *tmp_tiles, cudaStream_t st,
+                           int64_t *launches) {
+    const int64_t ntiles = (n + kScanTile - 1) / kScanTile > 0 ? (n + kScanTile - 1) / kScanTile : 1;
+    scan_tile_sums<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tmp_tiles);
+    scan_tile_offsets<<<1, kScanThreads, 0, st>>>(tmp_tiles, ntiles);
+    scan_tiles<<<(unsigned)ntiles, kScanThreads, 0, st>>>(in, n, tmp_tiles, out);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+int64_t scan_tmp_elems(int64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+// ---------------------------------------------------------------- fill G
+// warp per row: copy the fixed-stride scratch row (already sorted) into CSR.
+__global__ void fill_rows_kernel(int64_t n_rows, const int32_t *scol, const double *sval, int32_t stride,
+                                 const int64_t *rowptr, int32_t *col, double *val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+        const int64_t o = rowptr[r];
+        const int k = (int)(rowptr[r + 1] - o);
+        const int32_t *sc = scol + r * stride;
+        const double *sv = sval + r * stride;
+        for (int t = lane; t < k; t += 32) {
+            col[o + t] = sc[t];
+            val[o + t] = sv[t];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- transpose
+// count entries per column (columns mapped to [0, n_out) by subtracting col_lo)
+__global__ void count_cols_kernel(int64_t nnz, const int32_t *col, int64_t col_lo, int64_t n_out, int32_t *cnt) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = tid; e < nnz; e += nt) {
+        const int64_t c = (int64_t)col[e] - col_lo;
+        if (c >= 0 && c < n_out) atomicAdd(&cnt[c], 1);
+    }
+}
+
+// scatter entry (row, c, v) to rowptr_t[c] + cursor; order within a row fixed later
+__global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int64_t col_lo, int64_t n_out, const int64_t *t_rowptr,
+                                 int32_t *cursor, int32_t *t_col, double *t_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+        for (int64_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+            const int64_t c = (int64_t)col[e] - col_lo;
+            if (c < 0 || c >= n_out) continue;
+            const int p = atomicAdd(&cursor[c], 1);
+            t_col[t_rowptr[c] + p] = (int32_t)(r + row_begin);
+            t_val[t_rowptr[c] + p] = val[e];
+        }
+    }
+}
+
+// warp per row of G^T: rank sort by column (row index of G), ascending (C10)
+__global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *in_col, const double *in_val,
+                                 int32_t *out_col, double *out_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+        const int64_t o = rowptr[r];
+        const int k = (int)(rowptr[r + 1] - o);
+        for (int t = lane; t < k; t += 32) {
+            const int32_t c = in_col[o + t];
+            int rank = 0;
+            for (int u = 0; u < k; ++u) rank += (in_col[o + u] < c);
+            out_col[o + rank] = c;
+            out_val[o + rank] = in_val[o + t];
+        }
+    }
+}
+
+}  // namespace afsai

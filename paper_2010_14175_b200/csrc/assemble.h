@@ -1,0 +1,24 @@
+// Launch interface of assemble.cu
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace afsai {
+__global__ void validate_rows_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                     int64_t n_rows, int64_t row_begin, int64_t n_cols, unsigned long long *err);
+__global__ void row_len_max_kernel(const int64_t *rowptr, int64_t n_rows, unsigned long long *out);
+__global__ void symmetry_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                int64_t n_rows, int64_t row_begin, unsigned long long *err);
+cudaError_t exclusive_scan(const int32_t *in, int64_t n, int64_t *out, int64_t *tmp_tiles, cudaStream_t st,
+                           int64_t *launches);
+int64_t scan_tmp_elems(int64_t n);
+__global__ void fill_rows_kernel(int64_t n_rows, const int32_t *scol, const double *sval, int32_t stride,
+                                 const int64_t *rowptr, int32_t *col, double *val);
+__global__ void count_cols_kernel(int64_t nnz, const int32_t *col, int64_t col_lo, int64_t n_out, int32_t *cnt);
+__global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int64_t col_lo, int64_t n_out, const int64_t *t_rowptr,
+                                 int32_t *cursor, int32_t *t_col, double *t_val);
+__global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *in_col, const double *in_val,
+                                 int32_t *out_col, double *out_val);
+}  // namespace afsai

@@ -1,0 +1,237 @@
+// spmv.cu -- CSR SpMV for A p, G r and G^T t and the
+// PCG vector kernels.  HBM-bound: every kernel streams its operands once.
+//
+// SpMV: a "miniwarp" of W lanes per row (the group size
+// follows the mean nnz per row), lanes stride the row's entries so each group
+// load is coalesced, then a fixed xor-shuffle tree reduces the W partial sums.
+// Dot products needed by PCG are fused into the kernel that produces their
+// operand; each block writes one partial and the LAST block to finish reduces
+// all partials in index order (deterministic, no extra launch) and applies the
+// PCG scalar update (alpha, convergence test, beta).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "afsai_internal.h"
+#include "spmv.h"
+
+namespace afsai {
+
+constexpr unsigned kFullS = 0xffffffffu;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullS, v, o);
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = (lane < nw) ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(kFullS, r, o);
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+// Deterministic grid reduction: the last block reduces partials[0..gridDim.x) in
+// index order.  Returns true in thread 0 of the last block with *total set.
+__device__ __forceinline__ bool grid_reduce_last(double mine, double *partials, unsigned *counter, double *sh,
+                                                 double *total) {
+    __shared__ bool last;
+    const double b = block_sum(mine, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = b;
+        __threadfence();
+        const unsigned t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+    double s = 0.0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) s += ((volatile double *)partials)[k];
+    const double tot = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+        *total = tot;
+        *counter = 0u;
+        return true;
+    }
+    return false;
+}
+
+// y[row] = sum_e val[e] * x[col[e] - x_off]; optional fused dot sum_row y[row]*w[row]
+template <int W, int MODE>
+__global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
+    __shared__ double sh[32];
+    if (a.st && a.st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (W - 1);
+    constexpr int RPW = 32 / W;  // rows per warp per pass
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double dsum = 0.0;
+    for (int64_t r0 = warp * RPW; r0 < a.n; r0 += nwarps * RPW) {
+        const int64_t row = r0 + lane / W;
+        double acc = 0.0;
+        if (row < a.n) {
+            const int64_t e1 = a.rowptr[row + 1];
+            for (int64_t e = a.rowptr[row] + sub; e < e1; e += W)
+                acc = fma(__ldg(a.val + e), __ldg(a.x + (__ldg(a.col + e) - a.x_off)), acc);
+        }
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFullS, acc, o);
+        if (sub == 0 && row < a.n) {
+            a.y[row] = acc;
+            if (MODE != 0) dsum = fma(acc, a.w[row], dsum);
+        }
+    }
+    if (MODE == 0) return;
+    double tot;
+    if (grid_reduce_last(dsum, a.partials, a.counter, sh, &tot)) {
+        PcgState *s = a.st;
+        if (MODE == 1) {          // tot = p.q  ->  alpha = (r,z)/(p,q)
+            s->pq = tot;
+            s->alpha = s->rz / tot;
+        } else if (MODE == 2) {   // tot = r.z (new) -> beta
+            s->beta = tot / s->rz;
+            s->rz = tot;
+        } else if (MODE == 3) {   // initial r.z
+            s->rz = tot;
+        }
+    }
+}
+
+template <int W>
+static void launch_w(const SpmvArgs &a, int mode, int grid, cudaStream_t st) {
+    switch (mode) {
+        case 0: spmv_kernel<W, 0><<<grid, 256, 0, st>>>(a); break;
+        case 1: spmv_kernel<W, 1><<<grid, 256, 0, st>>>(a); break;
+        case 2: spmv_kernel<W, 2><<<grid, 256, 0, st>>>(a); break;
+        default: spmv_kernel<W, 3><<<grid, 256, 0, st>>>(a); break;
+    }
+}
+
+int spmv_group_width(double avg_nnz) {
+    // miniwarp size: the power of two nearest the mean row length, 4..32
+    int w = 4;
+    while (w < 32 && w < avg_nnz * 0.75) w <<= 1;
+    return w;
+}
+
+void launch_spmv(const SpmvArgs &a, int mode, int width, int grid, cudaStream_t st) {
+    switch (width) {
+        case 4: launch_w<4>(a, mode, grid, st); break;
+        case 8: launch_w<8>(a, mode, grid, st); break;
+        case 16: launch_w<16>(a, mode, grid, st); break;
+        default: launch_w<32>(a, mode, grid, st); break;
+    }
+}
+
+// ---------------------------------------------------------------- PCG vectors
+// x = 0, r = b, partial b.b -> st->bnorm2
+__global__ void __launch_bounds__(256) pcg_init_kernel(int64_t n, const double *b, double *x, double *r,
+                                                       double *partials, unsigned *counter, PcgState *st) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = b[k];
+        x[k] = 0.0;
+        r[k] = v;
+        s = fma(v, v, s);
+    }
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) {
+        st->bnorm2 = tot;
+        st->iters = 0;
+        st->done = (tot == 0.0) ? 1 : 0;
+        st->rel = (tot == 0.0) ? 0.0 : 1.0;
+    }
+}
+
+// x += alpha p; r -= alpha q; partial r.r -> convergence test (R12)
+__global__ void __launch_bounds__(256) pcg_axpy_kernel(int64_t n, double *x, double *r, const double *p,
+                                                       const double *q, double *partials, unsigned *counter,
+                                                       PcgState *st, double tol, int32_t max_iters) {
+    __shared__ double sh[32];
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        x[k] = fma(alpha, p[k], x[k]);
+        const double rk = fma(-alpha, q[k], r[k]);
+        r[k] = rk;
+        s = fma(rk, rk, s);
+    }
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) {
+        st->rr = tot;
+        st->iters += 1;
+        st->rel = sqrt(tot) / sqrt(st->bnorm2);
+        if (st->rel <= tol) st->done = 1;
+        else if (st->iters >= max_iters) st->done = 2;
+    }
+}
+
+// p = z + beta p
+__global__ void __launch_bounds__(256) pcg_update_p_kernel(int64_t n, double *p, const double *z, const PcgState *st,
+                                                           int first) {
+    if (st->done) return;
+    const double beta = first ? 0.0 : st->beta;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        p[k] = first ? z[k] : fma(beta, p[k], z[k]);
+}
+
+// r = b - A x (explicit residual at the end): y = A x computed by spmv first; here r = b - y, partial r.r
+__global__ void __launch_bounds__(256) residual_kernel(int64_t n, const double *b, const double *ax, double *partials,
+                                                       unsigned *counter, double *out) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double d = b[k] - ax[k];
+        s = fma(d, d, s);
+    }
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) *out = tot;
+}
+
+void launch_pcg_init(int64_t n, const double *b, double *x, double *r, double *partials, unsigned *counter,
+                     PcgState *st, int grid, cudaStream_t s) {
+    pcg_init_kernel<<<grid, 256, 0, s>>>(n, b, x, r, partials, counter, st);
+}
+void launch_pcg_axpy(int64_t n, double *x, double *r, const double *p, const double *q, double *partials,
+                     unsigned *counter, PcgState *st, double tol, int32_t max_iters, int grid, cudaStream_t s) {
+    pcg_axpy_kernel<<<grid, 256, 0, s>>>(n, x, r, p, q, partials, counter, st, tol, max_iters);
+}
+void launch_pcg_update_p(int64_t n, double *p, const double *z, const PcgState *st, int first, int grid,
+                         cudaStream_t s) {
+    pcg_update_p_kernel<<<grid, 256, 0, s>>>(n, p, z, st, first);
+}
+void launch_residual(int64_t n, const double *b, const double *ax, double *partials, unsigned *counter, double *out,
+                     int grid, cudaStream_t s) {
+    residual_kernel<<<grid, 256, 0, s>>>(n, b, ax, partials, counter, out);
+}
+
+// ---------------------------------------------------------------- fp64 FMA probe
+// Independent DFMA chains per thread (8 accumulators), enough warps to fill
+// every SMSP: the measured fp64 roofline denominator of the set-up.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double *out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-9, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+           x7 = x0 + 7;
+    for (int k = 0; k < iters; ++k) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double s = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+    if (s == 1234.5678) out[0] = s;  // keep the chains alive
+}
+
+void launch_dfma_probe(double *out, int iters, int grid, cudaStream_t s) {
+    dfma_probe_kernel<<<grid, 256, 0, s>>>(out, iters, 0.999999999, 1e-12);
+}
+
+}  // namespace afsai

@@ -1,0 +1,208 @@
+"""GPU vs oracle parity through the C ABI.
+
+Set-up: patterns identical and G within 1e-10 row-relative (BASELINE.json
+north_star); under the arithmetic contract C1-C12 we also expect, and assert,
+bitwise equality.  Trace (steps, stop reasons) equal.  G^T bitwise.  Apply
+within the SpMV rounding bound.  PCG iterations within +-1.
+"""
+import numpy as np
+import pytest
+import torch
+
+import afsai_inputs as ai
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.fail("no GPU")
+    from paper_2010_14175_b200.api import Context
+    c = Context()
+    yield c
+    c.close()
+
+
+def gpu_setup(ctx, A, nsteps, s, eps=0.0, cap=1 << 30):
+    from paper_2010_14175_b200.api import DeviceCSR, Factor
+    F = Factor(ctx, DeviceCSR.from_numpy(A), nsteps, s, eps, cap)
+    return F
+
+
+def host_csr(F, which=0):
+    rp, ci, v = F.G() if which == 0 else F.Gt()
+    return ai.CSR(rp.numel() - 1, rp.cpu().numpy(), ci.cpu().numpy(), v.cpu().numpy())
+
+
+def compare_rows(Gg, ref, rows, label):
+    """Per-row parity: pattern identical (else flagged iff the oracle margin < 1e-12),
+    values row-relative <= 1e-10, plus a count of non-bitwise rows."""
+    failed, flagged, nonbit = [], [], 0
+    for t, i in enumerate(rows):
+        c0, v0 = ref.row(t)
+        a, b = Gg.rowptr[i], Gg.rowptr[i + 1]
+        c1, v1 = Gg.col[a:b], Gg.val[a:b]
+        if len(c0) != len(c1) or not np.array_equal(c0, c1):
+            mg = ref.margin[t, : max(1, ref.steps[t])]
+            if np.nanmin(mg) < 1e-12:
+                flagged.append(int(i))
+            else:
+                failed.append(int(i))
+            continue
+        rel = np.max(np.abs(v1 - v0)) / np.max(np.abs(v0))
+        if rel > 1e-10:
+            failed.append(int(i))
+        if not np.array_equal(v0.view(np.int64), v1.view(np.int64)):
+            nonbit += 1
+    assert not failed, f"{label}: {len(failed)} rows fail parity, first {failed[:10]}"
+    return flagged, nonbit
+
+
+CASES = [
+    ("M1_poisson2d_32", lambda: ai.poisson2d(32, 32), 10, 1, 0.0, 1 << 30),
+    ("poisson3d_12_20x2", lambda: ai.poisson3d(12), 20, 2, 0.0, 1 << 30),
+    ("hetero_10_20x2", lambda: ai.hetero_poisson3d(10), 20, 2, 0.0, 1 << 30),
+    ("fe_5_30x3_cap100", lambda: ai.fe_elasticity(5), 30, 3, 0.0, 100),
+    ("rsparse_cap12_s5", lambda: ai.random_sparse_spd(3000, 10, sub=4), 6, 5, 0.0, 12),
+    ("rsparse_banded_s8", lambda: ai.random_sparse_spd(2000, 6, sub=5, bandwidth=40), 8, 8, 0.0, 1 << 30),
+    ("poisson3d_8_eps095", lambda: ai.poisson3d(8), 20, 2, 0.95, 1 << 30),
+    ("poisson2d_kmax0", lambda: ai.poisson2d(9, 7), 0, 1, 0.0, 1 << 30),
+    ("tridiag_64_k7", lambda: ai.tridiag(64), 7, 1, 0.0, 1 << 30),
+    ("dense50_full", lambda: ai.from_dense(ai.random_spd_dense(50, sub=50)), 50, 1, 0.0, 1 << 30),
+    ("dense90_s16", lambda: ai.from_dense(ai.random_spd_dense(90, sub=90)), 8, 16, 0.0, 1 << 30),
+    ("dense130_cap129", lambda: ai.from_dense(ai.random_spd_dense(130, sub=130)), 200, 1, 0.0, 129),
+    ("single_row", lambda: ai.diagonal([3.0]), 5, 2, 0.0, 1 << 30),
+]
+
+
+@pytest.mark.parametrize("name,make,k,s,eps,cap", CASES, ids=[c[0] for c in CASES])
+def test_setup_parity(ctx, name, make, k, s, eps, cap):
+    A = make()
+    F = gpu_setup(ctx, A, k, s, eps, cap)
+    G = host_csr(F)
+    ref = oracle.setup(A, k, s, eps, cap)
+    rows = np.arange(A.n)
+    flagged, nonbit = compare_rows(G, ref, rows, name)
+    assert not flagged, f"{name}: flagged rows under the contract: {flagged[:10]}"
+    assert nonbit == 0, f"{name}: {nonbit} rows not bitwise equal"
+    Gr = ref.to_csr(A.n)
+    assert np.array_equal(G.rowptr, Gr.rowptr)
+    st, rs = F.trace()
+    assert np.array_equal(st.cpu().numpy(), ref.steps)
+    assert np.array_equal(rs.cpu().numpy(), ref.reason)
+    stats = F.stats()
+    assert stats["nnz_G"] == Gr.nnz
+    assert sum(stats["rows_by_reason"]) == A.n
+    # transpose: exact, rows ascending (C10)
+    T = host_csr(F, 1)
+    Tr = oracle.transpose(Gr)
+    assert np.array_equal(T.rowptr, Tr.rowptr) and np.array_equal(T.col, Tr.col)
+    assert np.array_equal(T.val.view(np.int64), Tr.val.view(np.int64))
+    F.close()
+
+
+def apply_tolerance(G, Gt, r):
+    """|dz| <= gamma * G^T(|G||r|) (+ same for the inner product), u = 2^-53, gamma ~ 64u:
+    the standard SpMV rounding bound with a factor covering row lengths <= ~60."""
+    u = 2.0 ** -53
+    Ga, Gta = abs(G.to_scipy()), abs(Gt.to_scipy())
+    inner = Ga @ np.abs(r)
+    return 2 * 64 * u * (Gta @ inner) + 1e-300
+
+
+@pytest.mark.parametrize("make,k,s", [(lambda: ai.poisson3d(16), 20, 2), (lambda: ai.fe_elasticity(5), 30, 3)])
+def test_apply_parity(ctx, make, k, s):
+    A = make()
+    F = gpu_setup(ctx, A, k, s, 0.0, 100)
+    G, Gt = host_csr(F), host_csr(F, 1)
+    r = ai.rng("vectors", 11).standard_normal(A.n)
+    z_ref = oracle.apply(G, Gt, r)
+    z = F.apply(torch.from_numpy(r).cuda()).cpu().numpy()
+    tol = apply_tolerance(G, Gt, r)
+    assert np.all(np.abs(z - z_ref) <= tol), np.max(np.abs(z - z_ref) / tol)
+    # host buffers through the same C call (staged inside the library)
+    zh = torch.empty(A.n, dtype=torch.float64)
+    F.apply(torch.from_numpy(r), zh)
+    assert np.array_equal(zh.numpy(), z)
+    # preconditioner symmetry (u, M v) = (M u, v)
+    v = ai.rng("vectors", 12).standard_normal(A.n)
+    Mv = F.apply(torch.from_numpy(v).cuda()).cpu().numpy()
+    assert abs(r @ Mv - z @ v) <= 1e-12 * abs(r @ Mv)
+    F.close()
+
+
+@pytest.mark.parametrize("make,k,s,cap", [
+    (lambda: ai.poisson3d(16), 20, 2, 1 << 30),
+    (lambda: ai.poisson3d(16), 0, 1, 1 << 30),        # Jacobi (kmax = 0, P11)
+    (lambda: ai.hetero_poisson3d(12), 20, 2, 1 << 30),
+    (lambda: ai.fe_elasticity(6), 30, 3, 100),
+])
+def test_pcg_parity(ctx, make, k, s, cap):
+    A = make()
+    b, xs = ai.rhs_for(A)
+    F = gpu_setup(ctx, A, k, s, 0.0, cap)
+    x, rep = F.pcg(torch.from_numpy(b).cuda(), tol=1e-8, max_iters=5000)
+    G, Gt, _ = oracle.setup_full(A, k, s, 0.0, cap)
+    pr = oracle.pcg(A, G, Gt, b, tol=1e-8, max_iters=5000)
+    assert rep["converged"] and pr.converged
+    assert abs(rep["iters"] - pr.iters) <= 1, (rep["iters"], pr.iters)
+    assert rep["true_rel_res"] <= 10 * 1e-8
+    xg = x.cpu().numpy()
+    assert np.linalg.norm(xg - pr.x) <= 1e-6 * np.linalg.norm(pr.x)
+    F.close()
+
+
+def test_pcg_identity_and_host_buffers(ctx):
+    I = ai.diagonal(np.ones(100))
+    b = ai.rng("vectors", 13).standard_normal(100)
+    F = gpu_setup(ctx, I, 3, 1)
+    xh = torch.empty(100, dtype=torch.float64)
+    x, rep = F.pcg(torch.from_numpy(b), tol=1e-8, x=xh)   # host b and x
+    assert rep["iters"] == 1 and np.allclose(xh.numpy(), b, rtol=0, atol=1e-15)
+    F.close()
+
+
+def test_errors(ctx):
+    from paper_2010_14175_b200 import capi
+    # not SPD: [[1,2],[2,1]] -> ENOTSPD at row 1, step 1 (same as the oracle)
+    A = ai.from_dense(np.array([[1.0, 2.0], [2.0, 1.0]]))
+    with pytest.raises(capi.AfsaiError) as e:
+        gpu_setup(ctx, A, 3, 1)
+    assert e.value.code == capi.AFSAI_ENOTSPD and (e.value.row, e.value.step) == (1, 1)
+    # invalid: unsorted columns
+    B = ai.poisson2d(4, 4)
+    col = B.col.copy()
+    col[1], col[2] = col[2], col[1]
+    with pytest.raises(capi.AfsaiError) as e:
+        gpu_setup(ctx, ai.CSR(B.n, B.rowptr, col, B.val), 2, 1)
+    assert e.value.code == capi.AFSAI_EINVAL
+    # invalid params
+    with pytest.raises(capi.AfsaiError) as e:
+        gpu_setup(ctx, B, 2, 0)
+    assert e.value.code == capi.AFSAI_EINVAL
+    with pytest.raises(capi.AfsaiError) as e:
+        gpu_setup(ctx, B, 200, 2)   # mmax 400 > 128
+    assert e.value.code == capi.AFSAI_ELIMIT
+    # the context still works after errors
+    F = gpu_setup(ctx, B, 2, 1)
+    F.close()
+
+
+def test_host_csr_input(ctx):
+    """afsai_setup with HOST arrays (staged by the library) gives the same G."""
+    from paper_2010_14175_b200.api import DeviceCSR, Factor
+    A = ai.poisson3d(10)
+    Fh = Factor(ctx, DeviceCSR.from_numpy(A, device="cpu"), 20, 2)
+    Fd = Factor(ctx, DeviceCSR.from_numpy(A), 20, 2)
+    for a, b in zip(Fh.G(), Fd.G()):
+        assert torch.equal(a, b)
+
+
+def test_determinism_repeat(ctx):
+    A = ai.hetero_poisson3d(12)
+    G1 = [t.cpu() for t in gpu_setup(ctx, A, 20, 2).G()]
+    G2 = [t.cpu() for t in gpu_setup(ctx, A, 20, 2).G()]
+    for a, b in zip(G1, G2):
+        assert torch.equal(a, b)
