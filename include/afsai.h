@@ -111,6 +111,9 @@ typedef struct {
     int32_t rows_per_cta;        /* rows (warps) resident per CTA                     */
     int32_t retried_rows;        /* rows recomputed with a larger table               */
     int32_t halo_rows;           /* rows of A received from other ranks              */
+    int64_t phase_cycles[7];     /* SM cycles summed over warps in the set-up kernel:
+                                    prologue, gradient, select, gather, border, backsub, output */
+    int64_t max_universe;        /* largest candidate+pattern set of a row (table keys) */
 } afsai_setup_stats_t;
 
 typedef struct {

@@ -49,13 +49,16 @@ class afsai_setup_stats_t(ctypes.Structure):
                 ("grad_entries", ctypes.c_int64), ("ms_total", ctypes.c_double), ("ms_rows", ctypes.c_double),
                 ("ms_assemble", ctypes.c_double), ("ms_transpose", ctypes.c_double), ("ms_halo", ctypes.c_double),
                 ("table_size", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32), ("retried_rows", ctypes.c_int32),
-                ("halo_rows", ctypes.c_int32)]
+                ("halo_rows", ctypes.c_int32), ("phase_cycles", ctypes.c_int64 * 7),
+                ("max_universe", ctypes.c_int64)]
+
+    PHASES = ["prologue", "gradient", "select", "gather", "border", "backsub", "output"]
 
     def to_dict(self):
         d = {}
         for name, _ in self._fields_:
             v = getattr(self, name)
-            d[name] = list(v) if name == "rows_by_reason" else v
+            d[name] = list(v) if name in ("rows_by_reason", "phase_cycles") else v
         return d
 
 

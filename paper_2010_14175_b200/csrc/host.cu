@@ -240,6 +240,13 @@ const char *afsai_strerror(int code) {
 
 static int ctx_init(afsai_ctx_t c, void *stream, afsai_status_t *status) {
     AFSAI_CUDA_TRY(cudaGetDevice(&c->device));
+    // keep freed stream-ordered allocations cached in the device pool: the set-up
+    // scratch and G are re-allocated every call and remapping them costs ms
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     AFSAI_CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
     c->stream = (cudaStream_t)stream;
     for (auto &e : c->ev) AFSAI_CUDA_TRY(cudaEventCreate(&e));
@@ -445,10 +452,10 @@ int SetupWork::alloc(afsai_ctx_t ctx, int64_t n, int32_t mmax, afsai_status_t *s
         sval.alloc(nn * stride * sizeof(double), st) != cudaSuccess ||
         nnz_row.alloc(nn * sizeof(int32_t), st) != cudaSuccess || err.alloc(sizeof(unsigned long long), st) ||
         retry.alloc(nn * sizeof(int64_t), st) != cudaSuccess || retry_count.alloc(sizeof(int32_t), st) ||
-        work.alloc(sizeof(unsigned long long), st) || counters.alloc(16 * sizeof(unsigned long long), st))
+        work.alloc(sizeof(unsigned long long), st) || counters.alloc(32 * sizeof(unsigned long long), st))
         return set_status(status, AFSAI_ENOMEM, "set-up scratch");
     AFSAI_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), st));
-    AFSAI_CUDA_TRY(cudaMemsetAsync(counters.p, 0, 16 * sizeof(unsigned long long), st));
+    AFSAI_CUDA_TRY(cudaMemsetAsync(counters.p, 0, 32 * sizeof(unsigned long long), st));
     AFSAI_CUDA_TRY(cudaMemsetAsync(nnz_row.p, 0, nn * sizeof(int32_t), st));
     return AFSAI_OK;
 }
@@ -467,7 +474,7 @@ int SetupWork::check_error(afsai_ctx_t ctx, afsai_status_t *status) {
 }
 
 int SetupWork::read_stats(afsai_ctx_t ctx, afsai_setup_stats_t *s, afsai_status_t *status) {
-    unsigned long long c[16];
+    unsigned long long c[32];
     AFSAI_CUDA_TRY(cudaMemcpyAsync(c, counters.p, sizeof c, cudaMemcpyDeviceToHost, ctx->stream));
     AFSAI_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     s->steps_total = (int64_t)c[0];
@@ -476,6 +483,8 @@ int SetupWork::read_stats(afsai_ctx_t ctx, afsai_setup_stats_t *s, afsai_status_
     s->fma_grad = (int64_t)c[3];
     s->grad_entries = (int64_t)c[4];
     for (int r = 0; r < 4; ++r) s->rows_by_reason[r] = (int64_t)c[5 + r];
+    for (int k = 0; k < 7; ++k) s->phase_cycles[k] = (int64_t)c[9 + k];
+    s->max_universe = (int64_t)c[16];
     return AFSAI_OK;
 }
 

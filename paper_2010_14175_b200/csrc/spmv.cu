@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "afsai_internal.h"
 #include "spmv.h"
@@ -114,7 +115,14 @@ static void launch_w(const SpmvArgs &a, int mode, int grid, cudaStream_t st) {
 }
 
 int spmv_group_width(double avg_nnz) {
-    // miniwarp size: the power of two nearest the mean row length, 4..32
+    // miniwarp size chosen from the mean row length, 4..32;
+    // AFSAI_SPMV_WIDTH overrides (experiments)
+    static int forced = -1;
+    if (forced < 0) {
+        const char *e = std::getenv("AFSAI_SPMV_WIDTH");
+        forced = e ? std::atoi(e) : 0;
+    }
+    if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     int w = 4;
     while (w < 32 && w < avg_nnz * 0.75) w <<= 1;
     return w;
