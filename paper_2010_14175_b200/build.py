@@ -37,7 +37,7 @@ def _nccl_dirs():
 def _flags_for(src: str):
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
              "-Xptxas", "-v"] + ARCH
-    if os.path.basename(src) == "setup_kernel.cu":
+    if os.path.basename(src).startswith("setup_"):
         flags += ["-fmad=false"]
     return flags
 
@@ -49,19 +49,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "afsai.h")]
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
-    objs = []
+    objs, todo = [], []
     for s in srcs:
         o = os.path.join(OBJDIR, os.path.basename(s) + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
-            cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s)
-            r = subprocess.run(cmd, capture_output=True, text=True)
+            todo.append((s, o))
+
+    def compile_one(so):
+        s, o = so
+        cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        with open(os.path.join(OBJDIR, os.path.basename(s) + ".ptxas.txt"), "w") as f:
+            f.write(r.stderr)
+        return s, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        for s, r in ex.map(compile_one, todo):
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {s}")
-            log = os.path.join(OBJDIR, os.path.basename(s) + ".ptxas.txt")
-            with open(log, "w") as f:
-                f.write(r.stderr)
             if verbose:
                 sys.stderr.write(r.stderr)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):

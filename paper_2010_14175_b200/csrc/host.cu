@@ -136,11 +136,27 @@ static int ilog2(int x) {
 int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi, int64_t row_lo, int64_t nrows,
              const afsai_params_t &p, int32_t mmax, int64_t max_row_len, SetupWork &W, afsai_setup_stats_t *stats,
              afsai_status_t *status) {
-    // table size: twice an estimate of the candidate universe, power of two
-    const int64_t est = (int64_t)(mmax + 1) * (max_row_len + 1) / 2;
-    int H = 1 << std::max(6, ilog2((int)std::min<int64_t>(2 * est, 1 << 14)));
-    // prefer a small first table: universe estimates are pessimistic on stencils
-    H = std::min(H, 1 << std::max(6, ilog2(4 * (mmax + 1))));
+    // Kernel plan.  Short rows (stencils: max row length <= 9) use the hit-list
+    // kernel, whose gradient needs no loads of candidate rows; everything else and
+    // every retry uses the general kernel.  Lanes per row: 16 up to mmax 96, else 32.
+    // The candidate table starts small (stencil universes are small); rows that
+    // overflow an on-chip table are retried with 4x larger tables.
+    // AFSAI_LPR / AFSAI_TABLE / AFSAI_HITS=0 override (experiments).
+    int lpr = mmax <= 96 ? 16 : 32;
+    if (const char *e = std::getenv("AFSAI_LPR")) {
+        const int l = std::atoi(e);
+        if (l == 32 || (l == 16 && mmax <= 96)) lpr = l;
+    }
+    bool hits = max_row_len <= 9;  // one entry per lane at 16 lanes per row
+    if (const char *e = std::getenv("AFSAI_HITS")) hits = hits && std::atoi(e) != 0;
+    const int hc = max_row_len <= 7 ? 6 : 8;
+    int H = 1 << std::max(6, ilog2(4 * (mmax + 1)));
+    if (hits) H = 1 << std::max(6, ilog2(3 * (mmax + 1)));
+    if (const char *e = std::getenv("AFSAI_TABLE")) {
+        const int h = std::atoi(e);
+        if (h >= 64 && (h & (h - 1)) == 0) H = h;
+    }
+    int cact = 64;
     SetupKArgs a{};
     a.rowptr = Aext.rowptr;
     a.col = Aext.col;
@@ -176,17 +192,36 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         if (H > (1 << 15)) return set_status(status, AFSAI_ELIMIT, "candidate table would exceed 32768 slots");
         a.H = H;
         a.log2H = ilog2(H);
-        const int64_t wb = setup_warp_bytes(H, mmax, p.s);
-        a.warp_smem = (int32_t)wb;
-        int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / wb));
-        if (wb > 220 * 1024) return set_status(status, AFSAI_ELIMIT, "per-row state exceeds shared memory");
-        const int occ = std::max(1, setup_occupancy(mmax, p.s, wpc, (size_t)wb * wpc));
-        const int64_t warps_needed = (todo + 0);
+        a.cact = cact;
+        SetupKernFn f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
+        if (!f) return set_status(status, AFSAI_ELIMIT, "no kernel instance for this pattern size");
+        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc) : scan_row_bytes(H, mmax, p.s);
+        a.warp_smem = (int32_t)rb;
+        const int rpw = 32 / lpr;  // rows per warp
+        if (rb * rpw > 200 * 1024) return set_status(status, AFSAI_ELIMIT, "a warp's rows exceed shared memory");
+        // CTA size (1..8 warps) maximising the rows resident per SM
+        int wpc = 1, occ = 0, best = -1;
+        for (int wc = 1; wc <= 8; ++wc) {
+            const size_t sm_ = (size_t)rb * wc * rpw;
+            if (sm_ > 227 * 1024) break;
+            if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_) !=
+                cudaSuccess) { cudaGetLastError(); break; }
+            int o = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, (const void *)f, wc * 32, sm_) != cudaSuccess) {
+                cudaGetLastError();
+                break;
+            }
+            if (o * wc > best) { best = o * wc; wpc = wc; occ = o; }
+        }
+        const int rows_per_cta = wpc * rpw;
+        const size_t smem = (size_t)rb * rows_per_cta;
+        AFSAI_CUDA_TRY(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        occ = std::max(1, occ);
         int64_t grid = (int64_t)ctx->num_sms * occ;
-        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (warps_needed + wpc - 1) / wpc));
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (todo + rows_per_cta - 1) / rows_per_cta));
         if (first) {
             stats->table_size = H;
-            stats->rows_per_cta = wpc;
+            stats->rows_per_cta = rows_per_cta;
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
@@ -196,7 +231,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         }
         {
             KTimer kt(ctx, AFSAI_K_SETUP_ROWS);
-            AFSAI_CUDA_TRY(launch_setup_rows(a, wpc, (int)grid, ctx->stream));
+            f<<<(unsigned)grid, rows_per_cta * lpr, smem, ctx->stream>>>(a);
+            AFSAI_CUDA_TRY(cudaGetLastError());
         }
         ctx->launches += 1;
         int32_t rc = 0;
@@ -209,6 +245,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             AFSAI_CUDA_TRY(cudaMemcpyAsync(retry_in.p, W.retry.p, rc * sizeof(int64_t), cudaMemcpyDeviceToDevice,
                                            ctx->stream));
             H *= 4;
+            hits = false;  // retries use the general kernel
         }
         first = false;
     }

@@ -1,0 +1,270 @@
+// setup_common.cuh -- device code shared by the two per-row set-up kernels
+// (setup_scan.cu: general rows; setup_hits.cu: short rows with hit lists).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "afsai_internal.h"
+#include "setup_kernel.h"
+
+namespace afsai {
+
+constexpr int32_t kEmpty = -1;
+constexpr int8_t kCand = -2;
+constexpr int kGradChunk = 8;  // row entries loaded per batch in the gradient
+
+// lanes [base, base+LPR) of a warp working on one row
+template <int LPR>
+struct Group {
+    int gl;         // lane within the group
+    unsigned mask;  // the group's lanes
+    __device__ explicit Group(int lane)
+        : gl(lane & (LPR - 1)),
+          mask(LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane & ~(LPR - 1)))) {}
+    template <class T>
+    __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, LPR); }
+    template <class T>
+    __device__ __forceinline__ T xorv(T v, int o) const { return __shfl_xor_sync(mask, v, o, LPR); }
+    __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+    __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) v += xorv(v, o);
+        return v;
+    }
+    __device__ __forceinline__ unsigned long long sum(unsigned long long v) const {
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) v += xorv(v, o);
+        return v;
+    }
+};
+
+__device__ __forceinline__ uint32_t hslot(int32_t key, int log2H) {
+    return ((uint32_t)key * 2654435761u) >> (32 - log2H);
+}
+
+__device__ __forceinline__ int hfind(const int32_t *hkey, int H, int log2H, int32_t key) {
+    uint32_t msk = (uint32_t)H - 1u, sl = hslot(key, log2H);
+    for (int pr = 0; pr < H; ++pr) {
+        const int32_t k = hkey[sl];
+        if (k == key) return (int)sl;
+        if (k == kEmpty) return -1;
+        sl = (sl + 1u) & msk;
+    }
+    return -1;
+}
+
+// insert-if-absent; returns slot (or -1 if the table is full); *ins = newly inserted
+__device__ __forceinline__ int hinsert(int32_t *hkey, int H, int log2H, int32_t key, bool *ins) {
+    uint32_t msk = (uint32_t)H - 1u, sl = hslot(key, log2H);
+    for (int pr = 0; pr < H; ++pr) {
+        const int32_t k = hkey[sl];
+        if (k == key) { *ins = false; return (int)sl; }
+        if (k == kEmpty) {
+            const int32_t old = atomicCAS(&hkey[sl], kEmpty, key);
+            if (old == kEmpty) { *ins = true; return (int)sl; }
+            if (old == key) { *ins = false; return (int)sl; }
+        }
+        sl = (sl + 1u) & msk;
+    }
+    *ins = false;
+    return -1;
+}
+
+// strictly-lower packed row-major L: L[q][c], c < q, at q(q-1)/2 + c
+__device__ __forceinline__ int tri(int q) { return (q * (q - 1)) >> 1; }
+
+// (|a|, ja) better than (|b|, jb)?  |acc| descending, then column ascending.
+__device__ __forceinline__ bool better(double aa, int32_t ja, double ab, int32_t jb) {
+    return (aa > ab) || (aa == ab && ja < jb);
+}
+
+__device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) { return a.rowptr[r - a.a_lo] - a.base; }
+
+// Bordered Cholesky of the group of new rows q = qf .. qf+gs-1 (gathered rows in
+// arow/brow slots ug .. ug+gs-1), forward solve and psi update.
+//  - old columns c < qf: right-looking column sweep.  At stage k the owner lane
+//    of column k turns its accumulator into L[q][k] = t * inv[k] and broadcasts
+//    it; every lane folds fma(-L[q][k], L[c][k], t_c) into its own columns.
+//    Accumulators of already finalized columns are dead, so the fold runs
+//    unpredicated (their loads read the zero row to stay in bounds).
+//  - new columns (the diagonal of each new row and the couplings between new
+//    rows) are few: every lane keeps them redundantly, no broadcast needed.
+// Every accumulator folds in k-ascending order, exactly DESIGN.md C5.
+// Returns false on a pivot !(> 1e-30).
+template <int LPR, int NT, int GS, class State>
+__device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs, int ug, double &psi) {
+    const int M = w.M, gl = G.gl;
+    double t[GS][NT];
+    double dg[GS], ty[GS];
+    double cp[GS][GS];  // cp[u][v], v < u: accumulator of L[q_u][q_v]
+    double *Lnew[GS];
+    const double *Lr[NT];
+#pragma unroll
+    for (int u = 0; u < GS; ++u) {
+        const double *ar = w.arow + (ug + u) * M;
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt) {
+            const int c = gl + LPR * tt;
+            t[u][tt] = (u < gs && c < qf) ? ar[c] : 0.0;
+        }
+        dg[u] = (u < gs) ? ar[qf + u] : 0.0;
+#pragma unroll
+        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && u < gs) ? ar[qf + v] : 0.0;
+        ty[u] = (u < gs) ? -w.brow[ug + u] : 0.0;
+        Lnew[u] = w.L + tri(qf + u);
+    }
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        const int c = gl + LPR * tt;
+        Lr[tt] = (c < qf) ? w.L + tri(c) : w.zero;
+    }
+    // ---- stages over the old columns k < qf.  The shared-memory operands of
+    //      stage k+1 are loaded during stage k (software pipelining), so a stage's
+    //      critical path is DMUL -> SHFL -> DFMA only.
+    double inv_n = 0.0, y_n = 0.0, lsm_n[NT];
+#pragma unroll
+    for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = 0.0;
+    if (qf > 0) {
+        inv_n = w.inv[0];
+        y_n = w.y[0];
+#pragma unroll
+        for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][0];
+    }
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        int lnend = qf - LPR * tt;
+        if (lnend > LPR) lnend = LPR;
+        for (int ln = 0; ln < lnend; ++ln) {
+            const int k = LPR * tt + ln;
+            const double inv_k = inv_n;
+            const double y_k = y_n;
+            double lsm[NT];
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2) lsm[t2] = lsm_n[t2];
+            {
+                const int kn = (k + 1 < qf) ? k + 1 : k;  // prefetch (clamped, in bounds)
+                inv_n = w.inv[kn];
+                y_n = w.y[kn];
+#pragma unroll
+                for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];
+            }
+            double l[GS];
+#pragma unroll
+            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
+            if (gl == ln) {
+#pragma unroll
+                for (int u = 0; u < GS; ++u)
+                    if (u < gs) Lnew[u][k] = l[u];
+            }
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2)
+#pragma unroll
+                for (int u = 0; u < GS; ++u) t[u][t2] = fma(-l[u], lsm[t2], t[u][t2]);
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+                dg[u] = fma(-l[u], l[u], dg[u]);
+                ty[u] = fma(-l[u], y_k, ty[u]);
+#pragma unroll
+                for (int v = 0; v < GS; ++v)
+                    if (v < u) cp[u][v] = fma(-l[u], l[v], cp[u][v]);
+            }
+        }
+    }
+    // ---- the group's own columns k = qf + uf: finalize row uf, fold it into the
+    //      later group rows (all values redundant in every lane)
+#pragma unroll
+    for (int uf = 0; uf < GS; ++uf) {
+        if (uf >= gs) break;
+        const int k = qf + uf;
+        const double piv = dg[uf];
+        if (!(piv > 1e-30)) return false;
+        const double dq = sqrt(piv);  // C5.2: two correctly rounded operations
+        const double inv_k = 1.0 / dq;
+        const double y_k = ty[uf] * inv_k;
+        psi = fma(-y_k, y_k, psi);     // C6
+        if (gl == 0) {
+            w.inv[k] = inv_k;
+            w.y[k] = y_k;
+        }
+        double lu[GS];
+#pragma unroll
+        for (int u = 0; u < GS; ++u) {
+            lu[u] = 0.0;
+            if (u > uf && u < gs) {
+                lu[u] = cp[u][uf] * inv_k;
+                if (gl == 0) Lnew[u][k] = lu[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < GS; ++u) {
+            if (u > uf && u < gs) {
+                dg[u] = fma(-lu[u], lu[u], dg[u]);
+                ty[u] = fma(-lu[u], y_k, ty[u]);
+#pragma unroll
+                for (int v = 0; v < GS; ++v)
+                    if (v > uf && v < u) cp[u][v] = fma(-lu[u], lu[v], cp[u][v]);
+            }
+        }
+    }
+    G.sync();
+    return true;
+}
+
+// Back-substitution g~ = L^-T y (C7): descending column sweep; lane c
+// folds fma(-L[k][c], g[k], t_c) for k = m-1 down to c+1.  Accumulators with
+// c >= k are final (dead), so the fold is unpredicated; indices past the row are
+// clamped to stay inside L.
+template <int LPR, int NT, class State>
+__device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
+    const int gl = G.gl;
+    double tb[NT];
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        const int c = gl + LPR * tt;
+        tb[tt] = (c < m) ? w.y[c] : 0.0;
+    }
+    // operands of stage k-1 are loaded during stage k (software pipelining)
+    double iv_n = 0.0, lk_n[NT];
+#pragma unroll
+    for (int t2 = 0; t2 < NT; ++t2) lk_n[t2] = 0.0;
+    if (m > 0) {
+        const double *Lk = w.L + tri(m - 1);
+        iv_n = w.inv[m - 1];
+#pragma unroll
+        for (int t2 = 0; t2 < NT; ++t2) {
+            const int c = gl + LPR * t2;
+            lk_n[t2] = Lk[c < m - 1 ? c : 0];
+        }
+    }
+#pragma unroll
+    for (int tt = NT - 1; tt >= 0; --tt) {
+        int ln0 = m - 1 - LPR * tt;
+        if (ln0 > LPR - 1) ln0 = LPR - 1;
+        for (int ln = ln0; ln >= 0; --ln) {
+            const int k = LPR * tt + ln;
+            const double iv = iv_n;
+            double lk[NT];
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2) lk[t2] = lk_n[t2];
+            {
+                const int kn = k > 0 ? k - 1 : 0;
+                const double *Lk = w.L + tri(kn);
+                iv_n = w.inv[kn];
+#pragma unroll
+                for (int t2 = 0; t2 < NT; ++t2) {
+                    const int c = gl + LPR * t2;
+                    lk_n[t2] = Lk[c < kn ? c : 0];
+                }
+            }
+            const double gk = G.bcast(tb[tt] * iv, ln);
+            if (gl == ln) w.g[k] = gk;
+#pragma unroll
+            for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
+        }
+    }
+    G.sync();
+}
+
+}  // namespace afsai

@@ -1,4 +1,4 @@
-// Launch interface of the per-row set-up kernel (setup_kernel.cu).
+// Launch interface of the per-row set-up kernels (setup_scan.cu, setup_hits.cu).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -19,7 +19,8 @@ struct SetupKArgs {
     int32_t nsteps, s, cap, mmax;
     double eps;
     int32_t H, log2H;   // per-row hash table slots (power of two)
-    int32_t warp_smem;  // bytes of shared memory per warp (setup_warp_bytes)
+    int32_t cact;       // hit-list kernel: active candidate slots per row
+    int32_t warp_smem;  // bytes of shared memory per row (group)
     // outputs, index = global row - out_base
     int64_t out_base;
     int32_t stride;     // slots per row in the fixed-stride scratch (mmax + 1)
@@ -27,15 +28,21 @@ struct SetupKArgs {
     double *sval;
     int32_t *nnz_row, *steps, *reason;
     unsigned long long *err;       // packed (row << 24) | (step << 4) | code, atomicMin
-    int64_t *retry_rows;           // rows whose table overflowed
+    int64_t *retry_rows;           // rows whose on-chip tables overflowed
     int32_t *retry_count;
     unsigned long long *work;      // row queue counter
     unsigned long long *counters;  // [0] steps [1] fma_border [2] fma_backsub [3] fma_grad
                                    // [4] grad_entries [5..8] rows by stop reason
+                                   // [9..15] phase cycles [16] max universe
 };
 
-int64_t setup_warp_bytes(int H, int mmax, int s);
-cudaError_t launch_setup_rows(const SetupKArgs &a, int warps_per_cta, int grid, cudaStream_t st);
-int setup_occupancy(int mmax, int s, int warps_per_cta, size_t smem);
+using SetupKernFn = void (*)(SetupKArgs);
+
+// general kernel: candidates' rows of A re-read every step (any row length)
+SetupKernFn scan_kernel_for(int lpr, int mmax, int s);
+int64_t scan_row_bytes(int H, int mmax, int s);
+// hit-list kernel: rows of A with at most hc + 1 entries (stencils)
+SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);
+int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);
 
 }  // namespace afsai
