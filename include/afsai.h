@@ -162,6 +162,24 @@ int afsai_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z);
 int afsai_pcg(afsai_ctx_t ctx, const afsai_csr_t *A_local, afsai_factor_t F, const double *b, double *x,
               double tol, int32_t max_iters, afsai_pcg_report_t *rep, afsai_status_t *status);
 
+/* Set-up of the row block [row_lo, row_lo + n_rows) from A_ext, a CSR holding
+ * the rows [A_ext.row_begin, A_ext.row_begin + A_ext.n_rows) of the global A
+ * (global columns).  A_ext must contain every row the block's patterns can
+ * reach: with beta the bandwidth of A, the rows [row_lo - nsteps*beta, row_lo)
+ * below the block suffice.  The factor holds the block's rows of
+ * G (no G^T); they are bitwise equal to the same rows of a whole-matrix
+ * afsai_setup (row independence).  One GPU, no NCCL: the
+ * building block of the multi-GPU set-up, exposed for partition emulation. */
+int afsai_setup_block(afsai_ctx_t ctx, const afsai_csr_t *A_ext, int64_t row_lo, int64_t n_rows,
+                      const afsai_params_t *params, afsai_factor_t *out, afsai_status_t *status);
+
+/* Host-only halo planner (no GPU): ranks own [bounds[q], bounds[q+1]) and rank q
+ * needs the extended range [lo[q], hi[q]).  Writes rank `me`'s transfers as
+ * 4-tuples (kind 0 = send / 1 = recv, peer, global begin, count) into out and
+ * returns their number (-1 if max_out is too small). */
+int afsai_plan_ranges(int32_t me, int32_t nranks, const int64_t *bounds, const int64_t *lo, const int64_t *hi,
+                      int64_t *out, int32_t max_out);
+
 /* ---- factor access */
 int afsai_factor_nnz(afsai_factor_t F, int64_t *nnz_G, int64_t *nnz_Gt);
 /* Copy the local rows of G (which == 0) or G^T (which == 1) into caller buffers

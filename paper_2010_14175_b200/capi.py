@@ -22,6 +22,7 @@ EXPORTS = [
     "afsai_ctx_rank", "afsai_ctx_destroy", "afsai_setup", "afsai_apply", "afsai_pcg", "afsai_factor_nnz",
     "afsai_factor_copy", "afsai_factor_trace", "afsai_factor_stats", "afsai_factor_destroy",
     "afsai_ctx_launches", "afsai_probe_dfma_peak", "afsai_ctx_set_timing", "afsai_ctx_kernel_times",
+    "afsai_setup_block", "afsai_plan_ranges",
 ]
 KERNEL_CLASSES = ["setup_rows", "assemble", "transpose", "spmv_G", "spmv_Gt", "spmv_A", "vector", "comm"]
 
@@ -97,6 +98,9 @@ def load_library(path: str = LIB_PATH):
         "afsai_probe_dfma_peak": ([P, P, P], ctypes.c_int),
         "afsai_ctx_set_timing": ([P, i32], ctypes.c_int),
         "afsai_ctx_kernel_times": ([P, P, P], ctypes.c_int),
+        "afsai_setup_block": ([P, ctypes.POINTER(afsai_csr_t), i64, i64, ctypes.POINTER(afsai_params_t), P,
+                               ctypes.POINTER(afsai_status_t)], ctypes.c_int),
+        "afsai_plan_ranges": ([i32, i32, P, P, P, P, i32], ctypes.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)  # AttributeError if the symbol is missing
@@ -139,6 +143,7 @@ def make_csr(rowptr, col, val, n_cols: int, row_begin: int = 0) -> afsai_csr_t:
     c.rowptr = _ptr(rowptr).value if n_rows >= 0 else None
     c.col = _ptr(col).value
     c.val = _ptr(val).value
+    c._keep = (rowptr, col, val)  # the struct keeps its arrays alive
     return c
 
 
@@ -257,3 +262,30 @@ def afsai_ctx_kernel_times(ctx) -> dict:
     if rc:
         raise AfsaiError(rc, where="afsai_ctx_kernel_times")
     return {k: (int(la[i]), float(ms[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def afsai_setup_block(ctx, A_ext: afsai_csr_t, row_lo: int, n_rows: int, nsteps: int, s: int, eps: float,
+                      max_row_nnz: int):
+    p = afsai_params_t(nsteps, s, eps, max_row_nnz)
+    f = ctypes.c_void_p()
+    st = afsai_status_t()
+    rc = lib().afsai_setup_block(ctx, ctypes.byref(A_ext), int(row_lo), int(n_rows), ctypes.byref(p),
+                                 ctypes.byref(f), ctypes.byref(st))
+    if rc:
+        raise AfsaiError(rc, st, "afsai_setup_block")
+    return f
+
+
+def afsai_plan_ranges(me: int, nranks: int, bounds, lo, hi):
+    """Host-only halo plan: list of (kind 'send'|'recv', peer, begin, count)."""
+    import numpy as np
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    l = np.ascontiguousarray(lo, dtype=np.int64)
+    h = np.ascontiguousarray(hi, dtype=np.int64)
+    cap = 4 * nranks + 4
+    out = np.zeros(4 * cap, dtype=np.int64)
+    k = lib().afsai_plan_ranges(me, nranks, _ptr(b), _ptr(l), _ptr(h), _ptr(out), cap)
+    if k < 0:
+        raise AfsaiError(AFSAI_EINVAL, where="afsai_plan_ranges")
+    return [("send" if out[4 * t] == 0 else "recv", int(out[4 * t + 1]), int(out[4 * t + 2]), int(out[4 * t + 3]))
+            for t in range(k)]

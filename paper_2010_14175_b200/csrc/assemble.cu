@@ -247,4 +247,72 @@ __global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const in
     }
 }
 
+// ---------------------------------------------------------------- multi-GPU helpers
+// lengths of local rows (int32) from a row pointer
+__global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x)
+        len[r] = (int32_t)(rowptr[r + 1] - rowptr[r]);
+}
+
+// G entries -> (col, row, val) triples, row = global row of the entry
+__global__ void g_triples_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int32_t *tc, int32_t *tr, double *tv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw)
+        for (int64_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+            tc[e] = col[e];
+            tr[e] = (int32_t)(r + row_begin);
+            tv[e] = val[e];
+        }
+}
+
+// triples with col in [lo, hi) (one destination rank), compacted in input order
+// into out arrays at per-destination cursor; counts in cnt[dest]
+__global__ void count_dest_kernel(int64_t nnz, const int32_t *tc, const int64_t *bounds, int nranks,
+                                  unsigned long long *cnt) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = tc[e];
+        int q = 0;
+        while (q + 1 < nranks && c >= bounds[q + 1]) ++q;
+        atomicAdd(&cnt[q], 1ull);
+    }
+}
+
+__global__ void scatter_dest_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
+                                    const int64_t *bounds, int nranks, const unsigned long long *off,
+                                    unsigned long long *cur, int32_t *oc, int32_t *orow, double *ov) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = tc[e];
+        int q = 0;
+        while (q + 1 < nranks && c >= bounds[q + 1]) ++q;
+        const unsigned long long p = off[q] + atomicAdd(&cur[q], 1ull);
+        oc[p] = tc[e];
+        orow[p] = tr[e];
+        ov[p] = tv[e];
+    }
+}
+
+// G^T of a set of triples whose columns lie in [col_lo, col_lo + n_out):
+// count, (scan on host side), scatter, sort each row by source row (C10)
+__global__ void count_triples_kernel(int64_t nnz, const int32_t *tc, int64_t col_lo, int64_t n_out, int32_t *cnt) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = (int64_t)tc[e] - col_lo;
+        if (c >= 0 && c < n_out) atomicAdd(&cnt[c], 1);
+    }
+}
+
+__global__ void scatter_triples_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
+                                       int64_t col_lo, int64_t n_out, const int64_t *t_rowptr, int32_t *cursor,
+                                       int32_t *t_col, double *t_val) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = (int64_t)tc[e] - col_lo;
+        if (c < 0 || c >= n_out) continue;
+        const int p = atomicAdd(&cursor[c], 1);
+        t_col[t_rowptr[c] + p] = tr[e];
+        t_val[t_rowptr[c] + p] = tv[e];
+    }
+}
+
 }  // namespace afsai

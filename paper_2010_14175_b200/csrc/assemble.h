@@ -21,4 +21,16 @@ __global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const in
                                  int32_t *cursor, int32_t *t_col, double *t_val);
 __global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *in_col, const double *in_val,
                                  int32_t *out_col, double *out_val);
+__global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len);
+__global__ void g_triples_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int32_t *tc, int32_t *tr, double *tv);
+__global__ void count_dest_kernel(int64_t nnz, const int32_t *tc, const int64_t *bounds, int nranks,
+                                  unsigned long long *cnt);
+__global__ void scatter_dest_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
+                                    const int64_t *bounds, int nranks, const unsigned long long *off,
+                                    unsigned long long *cur, int32_t *oc, int32_t *orow, double *ov);
+__global__ void count_triples_kernel(int64_t nnz, const int32_t *tc, int64_t col_lo, int64_t n_out, int32_t *cnt);
+__global__ void scatter_triples_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
+                                       int64_t col_lo, int64_t n_out, const int64_t *t_rowptr, int32_t *cursor,
+                                       int32_t *t_col, double *t_val);
 }  // namespace afsai

@@ -838,6 +838,7 @@ int afsai_factor_stats(afsai_factor_t F, afsai_setup_stats_t *s) {
 void afsai_factor_destroy(afsai_factor_t F) {
     if (!F) return;
     cudaStreamSynchronize(F->ctx->stream);
+    dist_free(F);
     delete F;
 }
 

@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
             s->rz = tot;
         } else if (MODE == 3) {   // initial r.z
             s->rz = tot;
+        } else if (MODE == 4) {   // local dot for an all-reduce
+            s->sum[a.sum_idx] = tot;
         }
     }
 }
@@ -110,7 +112,8 @@ static void launch_w(const SpmvArgs &a, int mode, int grid, cudaStream_t st) {
         case 0: spmv_kernel<W, 0><<<grid, 256, 0, st>>>(a); break;
         case 1: spmv_kernel<W, 1><<<grid, 256, 0, st>>>(a); break;
         case 2: spmv_kernel<W, 2><<<grid, 256, 0, st>>>(a); break;
-        default: spmv_kernel<W, 3><<<grid, 256, 0, st>>>(a); break;
+        case 3: spmv_kernel<W, 3><<<grid, 256, 0, st>>>(a); break;
+        default: spmv_kernel<W, 4><<<grid, 256, 0, st>>>(a); break;
     }
 }
 
@@ -223,6 +226,94 @@ void launch_residual(int64_t n, const double *b, const double *ax, double *parti
                      int grid, cudaStream_t s) {
     residual_kernel<<<grid, 256, 0, s>>>(n, b, ax, partials, counter, out);
 }
+
+// ---------------------------------------------------------------- multi-GPU PCG
+__global__ void __launch_bounds__(256) pcg_init_dist_kernel(int64_t n, const double *b, double *x, double *r,
+                                                            double *partials, unsigned *counter, PcgState *st) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = b[k];
+        x[k] = 0.0;
+        r[k] = v;
+        s = fma(v, v, s);
+    }
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) {
+        st->sum[1] = tot;
+        st->iters = 0;
+        st->done = 0;
+    }
+}
+
+__global__ void pcg_start_dist_kernel(PcgState *st) {
+    st->bnorm2 = st->sum[1];
+    st->rz = st->sum[2];
+    st->rel = st->bnorm2 == 0.0 ? 0.0 : 1.0;
+    if (st->bnorm2 == 0.0) st->done = 1;
+}
+
+__global__ void __launch_bounds__(256) pcg_axpy_dist_kernel(int64_t n, double *x, double *r, const double *p,
+                                                            const double *q, double *partials, unsigned *counter,
+                                                            PcgState *st) {
+    __shared__ double sh[32];
+    if (st->done) return;
+    const double alpha = st->rz / st->sum[0];
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        x[k] = fma(alpha, p[k], x[k]);
+        const double rk = fma(-alpha, q[k], r[k]);
+        r[k] = rk;
+        s = fma(rk, rk, s);
+    }
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) {
+        st->sum[1] = tot;
+        st->alpha = alpha;
+        st->pq = st->sum[0];
+    }
+}
+
+__global__ void pcg_check_dist_kernel(PcgState *st, double tol, int32_t max_iters) {
+    if (st->done) return;
+    st->rr = st->sum[1];
+    st->iters += 1;
+    st->rel = sqrt(st->rr) / sqrt(st->bnorm2);
+    if (st->rel <= tol) st->done = 1;
+    else if (st->iters >= max_iters) st->done = 2;
+}
+
+__global__ void __launch_bounds__(256) pcg_update_p_dist_kernel(int64_t n, double *p, const double *z,
+                                                                const PcgState *st, int first) {
+    if (st->done) return;
+    const double beta = first ? 0.0 : st->sum[2] / st->rz;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        p[k] = first ? z[k] : fma(beta, p[k], z[k]);
+}
+
+__global__ void pcg_rz_dist_kernel(PcgState *st) {
+    if (st->done) return;
+    st->beta = st->sum[2] / st->rz;
+    st->rz = st->sum[2];
+}
+
+void launch_pcg_init_dist(int64_t n, const double *b, double *x, double *r, double *partials, unsigned *counter,
+                          PcgState *st, int grid, cudaStream_t s) {
+    pcg_init_dist_kernel<<<grid, 256, 0, s>>>(n, b, x, r, partials, counter, st);
+}
+void launch_pcg_start_dist(PcgState *st, cudaStream_t s) { pcg_start_dist_kernel<<<1, 1, 0, s>>>(st); }
+void launch_pcg_axpy_dist(int64_t n, double *x, double *r, const double *p, const double *q, double *partials,
+                          unsigned *counter, PcgState *st, int grid, cudaStream_t s) {
+    pcg_axpy_dist_kernel<<<grid, 256, 0, s>>>(n, x, r, p, q, partials, counter, st);
+}
+void launch_pcg_check_dist(PcgState *st, double tol, int32_t max_iters, cudaStream_t s) {
+    pcg_check_dist_kernel<<<1, 1, 0, s>>>(st, tol, max_iters);
+}
+void launch_pcg_update_p_dist(int64_t n, double *p, const double *z, PcgState *st, int first, int grid,
+                              cudaStream_t s) {
+    pcg_update_p_dist_kernel<<<grid, 256, 0, s>>>(n, p, z, st, first);
+}
+void launch_pcg_rz_dist(PcgState *st, cudaStream_t s) { pcg_rz_dist_kernel<<<1, 1, 0, s>>>(st); }
 
 // ---------------------------------------------------------------- fp64 FMA probe
 // Independent DFMA chains per thread (8 accumulators), enough warps to fill

@@ -11,6 +11,7 @@ namespace afsai {
 struct PcgState {
     double rz, pq, rr, alpha, beta, bnorm2, rel, true_rr;
     int32_t iters, done;  // done: 0 running, 1 converged, 2 max_iters
+    double sum[4];        // multi-GPU: local dot products, all-reduced in place
 };
 
 struct SpmvArgs {
@@ -25,6 +26,7 @@ struct SpmvArgs {
     double *partials;        // gridDim.x doubles
     unsigned *counter;       // last-block counter (zero at rest)
     PcgState *st;            // optional: skip when st->done; scalar updates
+    int sum_idx;             // mode 4: local dot stored in st->sum[sum_idx]
 };
 
 int spmv_group_width(double avg_nnz);
@@ -39,5 +41,15 @@ void launch_pcg_update_p(int64_t n, double *p, const double *z, const PcgState *
 void launch_residual(int64_t n, const double *b, const double *ax, double *partials, unsigned *counter, double *out,
                      int grid, cudaStream_t s);
 void launch_dfma_probe(double *out, int iters, int grid, cudaStream_t s);
+// multi-GPU PCG pieces (scalars from all-reduced st->sum[])
+void launch_pcg_init_dist(int64_t n, const double *b, double *x, double *r, double *partials, unsigned *counter,
+                          PcgState *st, int grid, cudaStream_t s);      // sum[1] = local b.b
+void launch_pcg_start_dist(PcgState *st, cudaStream_t s);               // bnorm2 = sum[1], rz = sum[2]
+void launch_pcg_axpy_dist(int64_t n, double *x, double *r, const double *p, const double *q, double *partials,
+                          unsigned *counter, PcgState *st, int grid, cudaStream_t s);  // sum[1] = local r.r
+void launch_pcg_check_dist(PcgState *st, double tol, int32_t max_iters, cudaStream_t s);
+void launch_pcg_update_p_dist(int64_t n, double *p, const double *z, PcgState *st, int first, int grid,
+                              cudaStream_t s);
+void launch_pcg_rz_dist(PcgState *st, cudaStream_t s);                  // rz = sum[2]
 
 }  // namespace afsai

@@ -206,3 +206,34 @@ def test_determinism_repeat(ctx):
     G2 = [t.cpu() for t in gpu_setup(ctx, A, 20, 2).G()]
     for a, b in zip(G1, G2):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("make,k,s,cap", [(lambda: ai.hetero_poisson3d(12), 8, 2, 1 << 30),
+                                          (lambda: ai.fe_elasticity(6), 10, 3, 100),
+                                          (lambda: ai.poisson3d(14), 20, 2, 1 << 30)])
+def test_block_setup_partition_emulation(ctx, make, k, s, cap):
+    """Rows of a block computed from a halo-extended copy of A (rows [b - k*beta, e)
+    only) are bitwise the same rows of the whole-matrix set-up (pin P12 on the GPU:
+    the multi-GPU set-up's building block)."""
+    from paper_2010_14175_b200 import capi
+    from paper_2010_14175_b200.api import DeviceCSR
+    A = make()
+    F = gpu_setup(ctx, A, k, s, 0.0, cap)
+    G = host_csr(F)
+    beta = A.bandwidth()
+    n = A.n
+    for b, e in [(0, n // 3), (n // 3, 2 * n // 3), (2 * n // 3, n)]:
+        lo = max(0, b - k * beta)
+        X = DeviceCSR.from_numpy(A, row_begin=lo, n_rows=e - lo)
+        h = capi.afsai_setup_block(ctx.h, X.c(), b, e - b, k, s, 0.0, min(cap, 2**31 - 1))
+        nnz, _ = capi.afsai_factor_nnz(h)
+        rp = torch.empty(e - b + 1, dtype=torch.int64, device="cuda")
+        ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        v = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        capi.afsai_factor_copy(h, 0, rp, ci, v)
+        capi.afsai_factor_destroy(h)
+        a0, a1 = G.rowptr[b], G.rowptr[e]
+        assert np.array_equal(rp.cpu().numpy(), G.rowptr[b:e + 1] - a0)
+        assert np.array_equal(ci.cpu().numpy(), G.col[a0:a1])
+        assert np.array_equal(v.cpu().numpy().view(np.int64), G.val[a0:a1].view(np.int64))
+    F.close()
