@@ -106,7 +106,7 @@ def run_reference(args, rank, world):
     import oracle
     cores = os.cpu_count() or 1
     # bounded slab of the workload: NX x NX x nz, nz sized so each step is ~10-30 s of CPU
-    nz = max(2, min(args.nx, int(round(4 * cores / 8))))
+    nz = max(2, min(args.nx, int(round(40 * cores / 8))))
     A = ai.poisson3d(args.nx, args.nx, nz)
     b, _ = ai.rhs_for(A)
     times = []
@@ -142,7 +142,7 @@ def cpu_baseline_leg(args):
     import afsai_inputs as ai
     import oracle
     cores = os.cpu_count() or 1
-    nz = max(2, min(args.nx, int(round(4 * cores / 8))))
+    nz = max(2, min(args.nx, int(round(40 * cores / 8))))   # ~10-30 s of CPU work
     A = ai.poisson3d(args.nx, args.nx, nz)
     b, _ = ai.rhs_for(A)
     t0 = time.perf_counter()
