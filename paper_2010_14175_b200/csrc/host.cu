@@ -149,8 +149,17 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     }
     bool hits = max_row_len <= 9;  // one entry per lane at 16 lanes per row
     if (const char *e = std::getenv("AFSAI_HITS")) hits = hits && std::atoi(e) != 0;
+    // lockstep: ls_lpr lanes per row, 32/ls_lpr rows per warp (rows <= ls_lpr entries, s <= 4)
+    int ls_lpr = 16;
+    if (const char *e = std::getenv("AFSAI_LOCKSTEP_LPR")) ls_lpr = std::atoi(e) == 8 ? 8 : 16;
+    bool lockstep = hits && max_row_len <= ls_lpr && p.s <= 4;
+    if (const char *e = std::getenv("AFSAI_LOCKSTEP")) lockstep = lockstep && std::atoi(e) != 0;
+    const int lpr0 = lpr;
     const int hc = max_row_len <= 7 ? 6 : 8;
-    int H = 1 << std::max(6, ilog2(4 * (mmax + 1)));
+    // universe <= (pattern rows) x (row length); observed ~ (mmax+1) * len / 10
+    // for FE (700 of 91 x 81), ~2.2 (mmax+1) for 7-point stencils
+    int H = 1 << std::max(6, ilog2((int)std::min<int64_t>(1 << 13, std::max<int64_t>(
+                                     4 * (mmax + 1), (int64_t)(mmax + 1) * max_row_len / 6))));
     if (hits) H = 1 << std::max(6, ilog2(3 * (mmax + 1)));
     if (const char *e = std::getenv("AFSAI_TABLE")) {
         const int h = std::atoi(e);
@@ -193,7 +202,15 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         a.H = H;
         a.log2H = ilog2(H);
         a.cact = cact;
-        SetupKernFn f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
+        SetupKernFn f = nullptr;
+        if (hits && lockstep) {
+            f = lockstep_kernel_for(ls_lpr, mmax, p.s, hc);
+            if (f) lpr = ls_lpr;
+        }
+        if (!f) {
+            lpr = lpr0;
+            f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
+        }
         if (!f) return set_status(status, AFSAI_ELIMIT, "no kernel instance for this pattern size");
         const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc) : scan_row_bytes(H, mmax, p.s);
         a.warp_smem = (int32_t)rb;

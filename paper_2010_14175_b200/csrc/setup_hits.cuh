@@ -1,0 +1,93 @@
+// setup_hits.cuh -- per-row state of the hit-list set-up kernels (setup_hits.cu,
+// setup_lockstep.cu).
+#pragma once
+#include "setup_common.cuh"
+
+namespace afsai {
+
+struct HitState {
+    double *inv, *y, *g, *L, *arow, *brow, *dscr, *zero, *hv, *acc;
+    int64_t *gstart;
+    int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey;
+    int16_t *ahs, *afree;
+    int8_t *hval, *ahn, *ahq;
+    int M, CA;
+};
+
+template <int HC>
+__host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc) {
+    int64_t dbl = 3 * (int64_t)M + (M * (M - 1)) / 2 + 1 + (int64_t)S * M + S + 2 + M + 1 + (int64_t)CA * HC +
+                  (acc ? CA : 0);
+    int64_t i64 = S;
+    int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA;
+    int64_t i16 = 2 * (int64_t)CA;
+    int64_t i8 = (int64_t)H + CA + (int64_t)CA * HC;
+    int64_t b = dbl * 8 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
+    return (b + 15) & ~int64_t(15);
+}
+
+template <int HC>
+__device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, bool acc) {
+    HitState w;
+    const int H = a.H, M = a.mmax, S = a.s, CA = a.cact;
+    w.M = M;
+    w.CA = CA;
+    double *d = reinterpret_cast<double *>(base);
+    w.inv = d; d += M;
+    w.y = d; d += M;
+    w.g = d; d += M;
+    w.L = d; d += (M * (M - 1)) / 2 + 1;
+    w.arow = d; d += S * M;
+    w.brow = d; d += S;
+    w.dscr = d; d += 2;
+    w.zero = d; d += M + 1;
+    w.hv = d; d += CA * HC;  // [h][a]
+    w.acc = nullptr;
+    if (acc) { w.acc = d; d += CA; }
+    int64_t *l8 = reinterpret_cast<int64_t *>(d);
+    w.gstart = l8; l8 += S;
+    int32_t *ip = reinterpret_cast<int32_t *>(l8);
+    w.hkey = ip; ip += H;
+    w.P = ip; ip += M;
+    w.sel = ip; ip += S;
+    w.sela = ip; ip += S;
+    w.glen = ip; ip += S;
+    w.misc = ip; ip += 8;
+    w.akey = ip; ip += CA;
+    int16_t *sp = reinterpret_cast<int16_t *>(ip);
+    w.ahs = sp; sp += CA;
+    w.afree = sp; sp += CA;
+    int8_t *bp = reinterpret_cast<int8_t *>(sp);
+    w.hval = bp; bp += H;
+    w.ahn = bp; bp += CA;
+    w.ahq = bp;  // [h][a]
+    return w;
+}
+
+// misc: [0] keys inserted  [1] overflow  [2] active high-water  [3] free-stack size
+
+// Insert the hit (column r at pattern position q, value v) into active slot aa,
+// keeping the list sorted by r; q = -1 stands for r = i (always last).
+template <int HC>
+__device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int32_t r, double v) {
+    const int CA = w.CA;
+    int n = w.ahn[aa];
+    if (n >= HC) {
+        w.misc[1] = 1;
+        return;
+    }
+    int pos = n;
+    while (pos > 0) {
+        const int qp = w.ahq[(pos - 1) * CA + aa];
+        const int32_t rp = qp < 0 ? 0x7fffffff : w.P[qp];
+        if (rp <= r) break;
+        w.ahq[pos * CA + aa] = (int8_t)qp;
+        w.hv[pos * CA + aa] = w.hv[(pos - 1) * CA + aa];
+        --pos;
+    }
+    w.ahq[pos * CA + aa] = (int8_t)q;
+    w.hv[pos * CA + aa] = v;
+    w.ahn[aa] = (int8_t)(n + 1);
+}
+
+}  // namespace afsai

@@ -44,5 +44,7 @@ int64_t scan_row_bytes(int H, int mmax, int s);
 // hit-list kernel: rows of A with at most hc + 1 entries (stencils)
 SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);
 int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);
+// hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4, mmax <= 6*lpr)
+SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);
 
 }  // namespace afsai

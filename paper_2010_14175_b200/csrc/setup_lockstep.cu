@@ -1,0 +1,596 @@
+// setup_lockstep.cu -- hit-list set-up kernel, several rows per warp in LOCKSTEP.
+//
+// Same algorithm and arithmetic as setup_hits.cu (C1-C12), but the
+// 32/LPR rows of a warp advance together: every loop that contains a shuffle
+// or a warp barrier runs to the warp-uniform maximum of its trip count and
+// each row's updates are predicated (by selects, so the arithmetic of a live
+// row is exactly the unpredicated one).  Two things follow:
+//  - shuffles use the full warp mask (no per-shuffle convergence checks), and
+//  - every stage of the triangular sweeps does the work of all the warp's rows
+//    at once: with 8 lanes per row each lane folds up to 6 columns per stage,
+//    so the fixed per-stage cost (operand loads, the broadcast, the owner's
+//    store, the loop) is shared by four rows.
+// Used for short rows (<= LPR entries, stencils) and s <= 4.
+#include "setup_hits.cuh"
+
+namespace afsai {
+
+constexpr unsigned kAll = 0xffffffffu;
+
+template <int LPR>
+struct LGroup {
+    int gl;
+    __device__ explicit LGroup(int lane) : gl(lane & (LPR - 1)) {}
+    template <class T>
+    __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(kAll, v, src, LPR); }
+    template <class T>
+    __device__ __forceinline__ T xorv(T v, int o) const { return __shfl_xor_sync(kAll, v, o, LPR); }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) v += xorv(v, o);
+        return v;
+    }
+    __device__ __forceinline__ unsigned long long sum(unsigned long long v) const {
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) v += xorv(v, o);
+        return v;
+    }
+    // this group's bits of a full-warp ballot
+    __device__ __forceinline__ unsigned ballot(bool p) const {
+        const unsigned b = __ballot_sync(kAll, p) >> ((threadIdx.x & 31) & ~(LPR - 1));
+        return LPR == 32 ? b : (b & ((1u << LPR) - 1u));
+    }
+};
+
+__device__ __forceinline__ int warp_max(int v) { return (int)__reduce_max_sync(kAll, (unsigned)(v < 0 ? 0 : v)); }
+
+// scan_row_hits of setup_hits.cu with the slot allocation made warp-uniform
+template <int LPR, int HC>
+__device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H, int log2H, int32_t i, bool valid,
+                                 int32_t c, double v, int q, double *arow_u, double *brow_u) {
+    const int CA = w.CA;
+    const int32_t r = q < 0 ? i : w.P[q < w.M ? q : 0];
+    bool need = false;
+    int sl = -1;
+    if (valid) {
+        if (c == i) {
+            if (q >= 0) *brow_u = v;
+            else w.dscr[0] = v;
+        } else if (c < i) {
+            bool ins;
+            sl = hinsert(w.hkey, H, log2H, c, &ins);
+            if (sl < 0) w.misc[1] = 1;
+            else if (ins) need = true;
+            else {
+                const int st = w.hval[sl];
+                if (st >= 0) {
+                    if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
+                } else {
+                    hit_insert<HC>(w, -2 - st, q, r, v);     // existing candidate: new hit
+                }
+            }
+        }
+    }
+    const unsigned bal = G.ballot(need);
+    const int nf = w.misc[3], hw = w.misc[2];
+    G.sync();
+    if (need) {
+        const int rk = __popc(bal & ((1u << G.gl) - 1u));
+        const int aa = rk < nf ? w.afree[nf - 1 - rk] : hw + (rk - nf);
+        if (aa >= CA) {
+            w.misc[1] = 1;
+        } else {
+            w.hval[sl] = (int8_t)(-2 - aa);
+            w.akey[aa] = c;
+            w.ahs[aa] = (int16_t)sl;
+            w.ahn[aa] = 1;
+            w.ahq[aa] = (int8_t)q;
+            w.hv[aa] = v;
+        }
+        atomicAdd(&w.misc[0], 1);
+    }
+    const int k = __popc(bal);
+    if (G.gl == 0 && k) {
+        const int take = k < nf ? k : nf;
+        w.misc[3] = nf - take;
+        w.misc[2] = hw + (k - take);
+    }
+    G.sync();
+}
+
+// border_group of setup_common.cuh in lockstep: the old-column stages run to the
+// warp maximum qf_max; a row's updates happen only while live (active && k < qf).
+template <int LPR, int NT, int GS>
+__device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool active, int qf, int gs, int ug,
+                                int qf_max, double &psi) {
+    const int M = w.M, gl = G.gl;
+    double t[GS][NT];
+    double dg[GS], ty[GS];
+    double cp[GS][GS];
+    double *Lnew[GS];
+    const double *Lr[NT];
+#pragma unroll
+    for (int u = 0; u < GS; ++u) {
+        const double *ar = w.arow + (ug + u) * M;
+        const bool ur = active && u < gs;
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt) {
+            const int c = gl + LPR * tt;
+            t[u][tt] = (ur && c < qf) ? ar[c] : 0.0;
+        }
+        dg[u] = ur ? ar[qf + u] : 0.0;
+#pragma unroll
+        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && ur) ? ar[qf + v] : 0.0;
+        ty[u] = ur ? -w.brow[ug + u] : 0.0;
+        Lnew[u] = w.L + tri(qf + u < M ? qf + u : 0);
+    }
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        const int c = gl + LPR * tt;
+        Lr[tt] = (active && c < qf) ? w.L + tri(c) : w.zero;
+    }
+    const int qlim = (active && qf > 0) ? qf - 1 : 0;  // clamp for the operand prefetch
+    double inv_n = w.inv[0], y_n = w.y[0], lsm_n[NT];
+#pragma unroll
+    for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][0];
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        int lnend = qf_max - LPR * tt;
+        if (lnend > LPR) lnend = LPR;
+#pragma unroll 2
+        for (int ln = 0; ln < lnend; ++ln) {
+            const int k = LPR * tt + ln;
+            const bool live = active && k < qf;
+            const double inv_k = inv_n, y_k = y_n;
+            double lsm[NT];
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2) lsm[t2] = lsm_n[t2];
+            {
+                const int kn = (k + 1 < qlim) ? k + 1 : qlim;
+                inv_n = w.inv[kn];
+                y_n = w.y[kn];
+#pragma unroll
+                for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];
+            }
+            double l[GS];
+#pragma unroll
+            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
+            if (live && gl == ln) {
+#pragma unroll
+                for (int u = 0; u < GS; ++u)
+                    if (u < gs) Lnew[u][k] = l[u];
+            }
+            // t accumulators outside a row's live stages are dead (finalized old
+            // columns, or columns that are not old): updated unpredicated
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2)
+#pragma unroll
+                for (int u = 0; u < GS; ++u) t[u][t2] = fma(-l[u], lsm[t2], t[u][t2]);
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+                const double nd = fma(-l[u], l[u], dg[u]);
+                const double ny = fma(-l[u], y_k, ty[u]);
+                dg[u] = live ? nd : dg[u];
+                ty[u] = live ? ny : ty[u];
+#pragma unroll
+                for (int v = 0; v < GS; ++v)
+                    if (v < u) {
+                        const double nc = fma(-l[u], l[v], cp[u][v]);
+                        cp[u][v] = live ? nc : cp[u][v];
+                    }
+            }
+        }
+    }
+    // the group's own columns (no shuffles: per row, divergence allowed)
+    bool ok = true;
+    if (active) {
+#pragma unroll
+        for (int uf = 0; uf < GS; ++uf) {
+            if (uf >= gs) break;
+            const int k = qf + uf;
+            const double piv = dg[uf];
+            if (!(piv > 1e-30)) {
+                ok = false;
+                break;
+            }
+            const double dq = sqrt(piv);  // C5.2
+            const double inv_k = 1.0 / dq;
+            const double y_k = ty[uf] * inv_k;
+            psi = fma(-y_k, y_k, psi);     // C6
+            if (gl == 0) {
+                w.inv[k] = inv_k;
+                w.y[k] = y_k;
+            }
+            double lu[GS];
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+                lu[u] = 0.0;
+                if (u > uf && u < gs) {
+                    lu[u] = cp[u][uf] * inv_k;
+                    if (gl == 0) Lnew[u][k] = lu[u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+                if (u > uf && u < gs) {
+                    dg[u] = fma(-lu[u], lu[u], dg[u]);
+                    ty[u] = fma(-lu[u], y_k, ty[u]);
+#pragma unroll
+                    for (int v = 0; v < GS; ++v)
+                        if (v > uf && v < u) cp[u][v] = fma(-lu[u], lu[v], cp[u][v]);
+                }
+            }
+        }
+    }
+    G.sync();
+    return ok;
+}
+
+// back_substitute of setup_common.cuh in lockstep (stages to the warp maximum m_max)
+template <int LPR, int NT>
+__device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool active, int m, int m_max) {
+    const int gl = G.gl;
+    double tb[NT];
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt) {
+        const int c = gl + LPR * tt;
+        tb[tt] = (active && c < m) ? w.y[c] : 0.0;
+    }
+    const int mlim = (active && m > 0) ? m - 1 : 0;
+    double iv_n, lk_n[NT];
+    {
+        const int k0 = (m_max - 1 < mlim) ? m_max - 1 : mlim;
+        const int kk = k0 < 0 ? 0 : k0;
+        const double *Lk = w.L + tri(kk);
+        iv_n = w.inv[kk];
+#pragma unroll
+        for (int t2 = 0; t2 < NT; ++t2) {
+            const int c = gl + LPR * t2;
+            lk_n[t2] = Lk[c < kk ? c : 0];
+        }
+    }
+#pragma unroll
+    for (int tt = NT - 1; tt >= 0; --tt) {
+        int ln0 = m_max - 1 - LPR * tt;
+        if (ln0 > LPR - 1) ln0 = LPR - 1;
+#pragma unroll 2
+        for (int ln = ln0; ln >= 0; --ln) {
+            const int k = LPR * tt + ln;
+            const bool live = active && k < m;
+            const double iv = iv_n;
+            double lk[NT];
+#pragma unroll
+            for (int t2 = 0; t2 < NT; ++t2) lk[t2] = lk_n[t2];
+            {
+                int kn = k - 1 < mlim ? k - 1 : mlim;
+                kn = kn < 0 ? 0 : kn;
+                const double *Lk = w.L + tri(kn);
+                iv_n = w.inv[kn];
+#pragma unroll
+                for (int t2 = 0; t2 < NT; ++t2) {
+                    const int c = gl + LPR * t2;
+                    lk_n[t2] = Lk[c < kn ? c : 0];
+                }
+            }
+            const double gk = G.bcast(tb[tt] * iv, ln);
+            if (live && gl == ln) w.g[k] = gk;
+#pragma unroll
+            for (int t2 = 0; t2 <= tt; ++t2) {
+                const double nv = fma(-lk[t2], gk, tb[t2]);
+                tb[t2] = live ? nv : tb[t2];
+            }
+        }
+    }
+    G.sync();
+}
+
+template <int LPR, int NT, int GS, int HC>
+__global__ void __launch_bounds__(256, 1) afsai_setup_rows_lockstep_kernel(SetupKArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    constexpr int RPW = 32 / LPR;
+    const int lane = threadIdx.x & 31;
+    const LGroup<LPR> G(lane);
+    const int gl = G.gl;
+    HitState w = carve_hits<HC>(smem + (size_t)(threadIdx.x / LPR) * a.warp_smem, a, false);
+    const int H = a.H, log2H = a.log2H, CA = w.CA;
+    unsigned long long c_steps = 0, c_border = 0, c_back = 0, c_gfma = 0;
+    unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
+    long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int x = gl; x <= a.mmax; x += LPR) w.zero[x] = 0.0;
+    G.sync();
+    long long tph = clock64();
+#define PHASE(idx)                       \
+    {                                    \
+        const long long t1_ = clock64(); \
+        ph[idx] += t1_ - tph;            \
+        tph = t1_;                       \
+    }
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.work, (unsigned long long)RPW);
+        base = __shfl_sync(kAll, base, 0);
+        if ((int64_t)base >= a.nrows) break;  // warp-uniform
+        const int64_t tix = (int64_t)base + (lane / LPR);
+        const bool has = tix < a.nrows;
+        const int64_t i64 = has ? (a.rows ? a.rows[tix] : a.row_lo + tix) : 0;
+        const int32_t i = (int32_t)i64;
+        const int64_t orow = i64 - a.out_base;
+        const int64_t e0i = has ? rp_of(a, i64) : 0, e1i = has ? rp_of(a, i64 + 1) : 0;
+        tph = clock64();
+        for (int sl = gl; sl < H; sl += LPR) w.hkey[sl] = kEmpty;
+        for (int x = gl; x < CA; x += LPR) w.ahn[x] = 0;
+        if (gl == 0) {
+            w.misc[0] = 0;
+            w.misc[1] = 0;
+            w.misc[2] = 0;
+            w.misc[3] = 0;
+            w.dscr[0] = 0.0;
+        }
+        G.sync();
+        {
+            const bool vi = has && gl < (int)(e1i - e0i);
+            const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
+            const double xi = vi ? __ldg(a.val + e0i + gl) : 0.0;
+            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr);
+        }
+        const double a_ii = w.dscr[0];
+        const double psi0 = a_ii;
+        double psi = psi0;
+        int m = 0, steps = 0, reason = AFSAI_STOP_KMAX, fail_step = 0;
+        bool fail = false, overflow = has && (w.misc[1] != 0);
+        bool running = has && !overflow;
+        PHASE(0)
+        for (int k = 1; k <= a.nsteps; ++k) {
+            if (!__any_sync(kAll, running)) break;
+            int room = a.s;
+            if (a.cap - 1 - m < room) room = a.cap - 1 - m;
+            if (running && room <= 0) {
+                reason = AFSAI_STOP_CAP;
+                running = false;
+            }
+            // ---- gradient: fold of each active candidate's hits (C3); no shuffles inside
+            int nc = 0;
+            double ba[GS];
+            int32_t bj[GS], bt[GS];
+#pragma unroll
+            for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = 0x7fffffff; bt[q] = -1; }
+            if (running) {
+                const int hw = w.misc[2];
+                for (int aa = gl; aa < hw; aa += LPR) {
+                    const int n = w.ahn[aa];
+                    if (n == 0) continue;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int h = 0; h < HC; ++h) {
+                        if (h < n) {
+                            const int q = w.ahq[h * CA + aa];
+                            const double gv = q < 0 ? 1.0 : w.g[q];
+                            acc = fma(w.hv[h * CA + aa], gv, acc);
+                        }
+                    }
+                    c_gfma += n;
+                    if (acc != 0.0) {
+                        ++nc;
+                        double ca = fabs(acc);
+                        int32_t cj = w.akey[aa];
+                        int32_t ct = aa;
+#pragma unroll
+                        for (int q = 0; q < GS; ++q) {
+                            if (better(ca, cj, ba[q], bj[q])) {
+                                const double ta = ba[q];
+                                const int32_t tj = bj[q], t2 = bt[q];
+                                ba[q] = ca; bj[q] = cj; bt[q] = ct;
+                                ca = ta; cj = tj; ct = t2;
+                            }
+                        }
+                    }
+                }
+            }
+            nc = G.sum(nc);
+            PHASE(1)
+            if (running && nc == 0) {
+                reason = AFSAI_STOP_NOCAND;
+                running = false;
+            }
+            const int nsel = running ? (nc < room ? nc : room) : 0;
+            const int nsel_max = warp_max(nsel);
+            if (nsel_max == 0) continue;
+            // ---- selection: nsel_max rounds of group argmax over the list heads
+            for (int u = 0; u < nsel_max; ++u) {
+                double wa = ba[0];
+                int32_t wj = bj[0];
+#pragma unroll
+                for (int o = LPR / 2; o > 0; o >>= 1) {
+                    const double oa = G.xorv(wa, o);
+                    const int32_t oj = G.xorv(wj, o);
+                    if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
+                }
+                if (u < nsel && bj[0] == wj) {
+                    w.sel[u] = wj;
+                    w.sela[u] = bt[0];
+#pragma unroll
+                    for (int q = 0; q + 1 < GS; ++q) { ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1]; }
+                    ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                }
+            }
+            G.sync();
+            if (gl < nsel) {
+                const int32_t j = w.sel[gl];
+                int rank = 0;
+                for (int u = 0; u < nsel; ++u) rank += (w.sel[u] < j);
+                const int aa = w.sela[gl];
+                w.P[m + rank] = j;
+                w.hval[w.ahs[aa]] = (int8_t)(m + rank);
+                const int64_t g0 = rp_of(a, j), g1 = rp_of(a, (int64_t)j + 1);
+                w.gstart[rank] = g0;
+                w.glen[rank] = (int32_t)(g1 - g0);
+                w.ahn[aa] = 0;
+                w.afree[w.misc[3] + gl] = (int16_t)aa;
+            }
+            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = 0.0;
+            if (gl < nsel) w.brow[gl] = 0.0;
+            G.sync();
+            if (gl == 0) w.misc[3] += nsel;
+            G.sync();
+            PHASE(2)
+            // ---- gather: new rows (one entry per lane), all loads in flight first
+            for (int ug = 0; ug < nsel_max; ug += GS) {
+                int32_t pc[GS];
+                double pv[GS];
+                bool pvld[GS];
+#pragma unroll
+                for (int u = 0; u < GS; ++u) {
+                    pvld[u] = (ug + u < nsel) && gl < w.glen[ug + u];
+                    pc[u] = pvld[u] ? __ldg(a.col + w.gstart[ug + u] + gl) : 0;
+                    pv[u] = pvld[u] ? __ldg(a.val + w.gstart[ug + u] + gl) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < GS; ++u)
+                    if (ug + u < nsel_max)
+                        scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + ug + u,
+                                                  w.arow + ((ug + u) < a.s ? ug + u : 0) * w.M,
+                                                  w.brow + ((ug + u) < a.s ? ug + u : 0));
+            }
+            PHASE(3)
+            if (running && (w.misc[1] != 0 || w.misc[0] * 4 > H * 3)) {
+                overflow = true;
+                running = false;
+            }
+            // ---- bordered Cholesky of the new rows, groups of GS rows
+            for (int ug = 0; ug < nsel_max; ug += GS) {
+                int gs = running ? nsel - ug : 0;
+                gs = gs < 0 ? 0 : (gs > GS ? GS : gs);
+                const bool act = gs > 0;
+                const int qf_max = warp_max(act ? m + ug : 0);
+                if (!border_group_ls<LPR, NT, GS>(w, G, act, m + ug, gs, ug, qf_max, psi)) {
+                    fail = true;
+                    fail_step = k;
+                    running = false;
+                }
+            }
+            if (running) {
+                for (int u = 0; u < nsel; ++u) {
+                    const long q = m + u;
+                    c_border += (unsigned long long)(q * (q - 1) / 2 + 2 * q + 1);
+                }
+                m += nsel;
+                if (!(psi > 0.0)) {
+                    fail = true;
+                    fail_step = k;
+                    running = false;
+                }
+            }
+            PHASE(4)
+            // ---- back-substitution
+            const int m_max = warp_max(running ? m : 0);
+            back_substitute_ls<LPR, NT>(w, G, running, m, m_max);
+            if (running) {
+                c_back += (unsigned long long)(m * (m - 1) / 2);
+                steps = k;
+                if (psi / psi0 <= a.eps) {
+                    reason = AFSAI_STOP_TOL;
+                    running = false;
+                }
+            }
+            PHASE(5)
+        }
+        // ---- per-row outcome (no shuffles below until the final sync)
+        if (has) {
+            if (overflow) {
+                if (gl == 0) {
+                    const int p = atomicAdd(a.retry_count, 1);
+                    a.retry_rows[p] = i64;
+                }
+            } else if (fail) {
+                if (gl == 0) {
+                    const unsigned long long code = ((unsigned long long)i64 << 24) |
+                                                    ((unsigned long long)(fail_step & 0xfffff) << 4) |
+                                                    (unsigned long long)AFSAI_ENOTSPD;
+                    atomicMin(a.err, code);
+                    a.nnz_row[orow] = 0;
+                }
+            } else {
+                const double d = 1.0 / sqrt(psi);
+                int32_t *oc = a.scol + orow * a.stride;
+                double *ov = a.sval + orow * a.stride;
+#pragma unroll
+                for (int tt = 0; tt < NT; ++tt) {
+                    const int q = gl + LPR * tt;
+                    if (q < m) {
+                        const int32_t pj = w.P[q];
+                        int rank = 0;
+                        for (int q2 = 0; q2 < m; ++q2) rank += (w.P[q2] < pj);
+                        oc[rank] = pj;
+                        ov[rank] = w.g[q] * d;
+                    }
+                }
+                if (gl == 0) {
+                    oc[m] = i;
+                    ov[m] = d;
+                    a.nnz_row[orow] = m + 1;
+                    a.steps[orow] = steps;
+                    a.reason[orow] = reason;
+                    c_steps += steps;
+                    c_r0 += (reason == 0);
+                    c_r1 += (reason == 1);
+                    c_r2 += (reason == 2);
+                    c_r3 += (reason == 3);
+                    c_univ = max(c_univ, (unsigned long long)w.misc[0]);
+                }
+            }
+        }
+        G.sync();
+        PHASE(6)
+    }
+#undef PHASE
+    const unsigned long long g1 = G.sum(c_gfma);
+    if (gl == 0) {
+        atomicAdd(&a.counters[0], c_steps);
+        atomicAdd(&a.counters[1], c_border);
+        atomicAdd(&a.counters[2], c_back);
+        atomicAdd(&a.counters[3], g1);
+        atomicAdd(&a.counters[5], c_r0);
+        atomicAdd(&a.counters[6], c_r1);
+        atomicAdd(&a.counters[7], c_r2);
+        atomicAdd(&a.counters[8], c_r3);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) atomicAdd(&a.counters[9 + k], (unsigned long long)ph[k]);
+        atomicMax(&a.counters[16], c_univ);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <int LPR, int NT, int HC>
+static SetupKernFn ls_gs(int gs) {
+    switch (gs) {
+        case 1: return afsai_setup_rows_lockstep_kernel<LPR, NT, 1, HC>;
+        case 2: return afsai_setup_rows_lockstep_kernel<LPR, NT, 2, HC>;
+        case 3: return afsai_setup_rows_lockstep_kernel<LPR, NT, 3, HC>;
+        default: return afsai_setup_rows_lockstep_kernel<LPR, NT, 4, HC>;
+    }
+}
+
+template <int LPR, int HC>
+static SetupKernFn ls_nt(int nt, int gs) {
+    switch (nt) {
+        case 1: return ls_gs<LPR, 1, HC>(gs);
+        case 2: return ls_gs<LPR, 2, HC>(gs);
+        case 3: return ls_gs<LPR, 3, HC>(gs);
+        case 4: return ls_gs<LPR, 4, HC>(gs);
+        case 5: return ls_gs<LPR, 5, HC>(gs);
+        default: return ls_gs<LPR, 6, HC>(gs);
+    }
+}
+
+// lpr (8 or 16) lanes per row, 32/lpr rows per warp; rows <= lpr entries,
+// s <= 4, mmax <= 6 * lpr
+SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc) {
+    if (s > kMaxGroup || mmax > 6 * lpr) return nullptr;
+    const int m = mmax < 1 ? 1 : mmax;
+    const int nt = (m + lpr - 1) / lpr;
+    if (lpr == 8) return hc <= 6 ? ls_nt<8, 6>(nt, s) : ls_nt<8, 8>(nt, s);
+    return hc <= 6 ? ls_nt<16, 6>(nt, s) : ls_nt<16, 8>(nt, s);
+}
+
+}  // namespace afsai
