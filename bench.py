@@ -281,6 +281,8 @@ def main():
     apply_gbs = (bytes_G * la_G / max(ms_G, 1e-9) + 0) / 1e6 if ms_G > 0 else None
     extra = {
         "setup_ms": float(stats["ms_total"]),
+        "setup_phase_ms": {"rows_kernel": stats["ms_rows"], "assemble": stats["ms_assemble"],
+                           "transpose": stats["ms_transpose"], "halo": stats["ms_halo"]},
         "setup_rows_kernel_ms": setup_ms,
         "setup_gnnz_per_s": nnzG / (stats["ms_total"] * 1e-3) if stats["ms_total"] > 0 else None,
         "setup_fp64_tflops": setup_flop / (setup_ms * 1e-3) / 1e12 if setup_ms > 0 else None,

@@ -294,6 +294,37 @@ __global__ void scatter_dest_kernel(int64_t nnz, const int32_t *tc, const int32_
     }
 }
 
+// entries of the local G with column in [lo, hi): per-row counts, then (after a
+// scan of the counts) the (col, row, val) triples in row-major order
+__global__ void band_count_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, int64_t lo, int64_t hi,
+                                  int32_t *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        int c = 0;
+        for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+            const int64_t j = col[e];
+            c += (j >= lo && j < hi);
+        }
+        cnt[r] = c;
+    }
+}
+
+__global__ void band_fill_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int64_t lo, int64_t hi, const int64_t *off, int32_t *tc,
+                                 int32_t *tr, double *tv) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = off[r];
+        for (int64_t e = rowptr[r]; e < rowptr[r + 1]; ++e) {
+            const int64_t j = col[e];
+            if (j >= lo && j < hi) {
+                tc[p] = (int32_t)j;
+                tr[p] = (int32_t)(r + row_begin);
+                tv[p] = val[e];
+                ++p;
+            }
+        }
+    }
+}
+
 // G^T of a set of triples whose columns lie in [col_lo, col_lo + n_out):
 // count, (scan on host side), scatter, sort each row by source row (C10)
 __global__ void count_triples_kernel(int64_t nnz, const int32_t *tc, int64_t col_lo, int64_t n_out, int32_t *cnt) {

@@ -29,6 +29,11 @@ __global__ void count_dest_kernel(int64_t nnz, const int32_t *tc, const int64_t 
 __global__ void scatter_dest_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
                                     const int64_t *bounds, int nranks, const unsigned long long *off,
                                     unsigned long long *cur, int32_t *oc, int32_t *orow, double *ov);
+__global__ void band_count_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, int64_t lo, int64_t hi,
+                                  int32_t *cnt);
+__global__ void band_fill_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                                 int64_t row_begin, int64_t lo, int64_t hi, const int64_t *off, int32_t *tc,
+                                 int32_t *tr, double *tv);
 __global__ void count_triples_kernel(int64_t nnz, const int32_t *tc, int64_t col_lo, int64_t n_out, int32_t *cnt);
 __global__ void scatter_triples_kernel(int64_t nnz, const int32_t *tc, const int32_t *tr, const double *tv,
                                        int64_t col_lo, int64_t n_out, const int64_t *t_rowptr, int32_t *cursor,

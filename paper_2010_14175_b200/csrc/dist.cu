@@ -20,6 +20,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -238,117 +240,150 @@ static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<in
     return AFSAI_OK;
 }
 
-// G^T of the distributed G: route triples (j, i, g_ij) to owner(j), then
-// count / scan / scatter / sort on the receiving rank.
+// G^T of the distributed G.  G is lower triangular, so an entry (i, j) of a local
+// row lies either in a local G^T row (j >= b) or in a G^T row owned by a lower
+// rank.  Local entries go through the 1-GPU count / scan / scatter path; the
+// few entries for each lower rank q are extracted in row order (per-row
+// counts, scan, fill) and sent as (col, row, val) triples; received triples
+// (from higher ranks) join the local G^T rows, which are then sorted by row.
+struct DbgTimer {
+    bool on = false;
+    cudaStream_t st;
+    std::vector<cudaEvent_t> ev;
+    std::vector<const char *> nm;
+    explicit DbgTimer(cudaStream_t s) : st(s) { on = std::getenv("AFSAI_DEBUG_TIMING") != nullptr; }
+    void mark(const char *name) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        ev.push_back(e);
+        nm.push_back(name);
+    }
+    ~DbgTimer() {
+        if (!on || ev.empty()) return;
+        cudaEventSynchronize(ev.back());
+        for (size_t k = 1; k < ev.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[k - 1], ev[k]);
+            std::fprintf(stderr, "[afsai timing] %-28s %8.3f ms\n", nm[k], ms);
+        }
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<int64_t> &bounds,
                           afsai_status_t *status) {
     cudaStream_t st = ctx->stream;
+    DbgTimer dt(st);
+    dt.mark("start");
     const int np = ctx->nranks, me = ctx->rank;
-    const int64_t nnz = F->nnz_G, b = bounds[me], e = bounds[me + 1];
+    const int64_t b = bounds[me], e = bounds[me + 1], n = F->n_rows;
     const int grid = grid_stream(ctx);
-    DevBuf tc, tr, tv, dbounds, cnt, off, cur, sc, sr, sv;
-    AFSAI_CUDA_TRY(tc.alloc(std::max<int64_t>(nnz, 1) * 4, st));
-    AFSAI_CUDA_TRY(tr.alloc(std::max<int64_t>(nnz, 1) * 4, st));
-    AFSAI_CUDA_TRY(tv.alloc(std::max<int64_t>(nnz, 1) * 8, st));
-    AFSAI_CUDA_TRY(dbounds.alloc((np + 1) * 8, st));
-    AFSAI_CUDA_TRY(cnt.alloc(np * 8, st));
-    AFSAI_CUDA_TRY(off.alloc(np * 8, st));
-    AFSAI_CUDA_TRY(cur.alloc(np * 8, st));
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(dbounds.p, bounds.data(), (np + 1) * 8, cudaMemcpyHostToDevice, st));
-    AFSAI_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, np * 8, st));
-    AFSAI_CUDA_TRY(cudaMemsetAsync(cur.p, 0, np * 8, st));
-    g_triples_kernel<<<grid, 256, 0, st>>>(F->n_rows, F->g_rowptr.as<int64_t>(), F->g_col.as<int32_t>(),
-                                           F->g_val.as<double>(), F->row_begin, tc.as<int32_t>(), tr.as<int32_t>(),
-                                           tv.as<double>());
-    count_dest_kernel<<<grid, 256, 0, st>>>(nnz, tc.as<int32_t>(), dbounds.as<int64_t>(), np,
-                                            cnt.as<unsigned long long>());
-    ctx->launches += 2;
-    std::vector<unsigned long long> hc(np), hoff(np);
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(hc.data(), cnt.p, np * 8, cudaMemcpyDeviceToHost, st));
-    AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
-    unsigned long long acc = 0;
-    for (int q = 0; q < np; ++q) {
-        hoff[q] = acc;
-        acc += hc[q];
+    const int64_t *grp = F->g_rowptr.as<int64_t>();
+    const int32_t *gci = F->g_col.as<int32_t>();
+    const double *gv = F->g_val.as<double>();
+    // ---- outgoing triples, one contiguous buffer per lower rank
+    DevBuf rc32, roff, tiles_r;
+    AFSAI_CUDA_TRY(rc32.alloc(std::max<int64_t>(n, 1) * 4, st));
+    AFSAI_CUDA_TRY(roff.alloc((n + 1) * 8, st));
+    AFSAI_CUDA_TRY(tiles_r.alloc(scan_tmp_elems(n) * 8 + 16, st));
+    std::vector<int64_t> scnt(np, 0);
+    std::vector<DevBuf> sc(np), sr(np), sv(np);
+    for (int q = 0; q < me; ++q) {
+        band_count_kernel<<<grid, 256, 0, st>>>(n, grp, gci, bounds[q], bounds[q + 1], rc32.as<int32_t>());
+        AFSAI_CUDA_TRY(exclusive_scan(rc32.as<int32_t>(), n, roff.as<int64_t>(), tiles_r.as<int64_t>(), st,
+                                      &ctx->launches));
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(&scnt[q], roff.as<int64_t>() + n, 8, cudaMemcpyDeviceToHost, st));
+        AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+        AFSAI_CUDA_TRY(sc[q].alloc(std::max<int64_t>(scnt[q], 1) * 4, st));
+        AFSAI_CUDA_TRY(sr[q].alloc(std::max<int64_t>(scnt[q], 1) * 4, st));
+        AFSAI_CUDA_TRY(sv[q].alloc(std::max<int64_t>(scnt[q], 1) * 8, st));
+        band_fill_kernel<<<grid, 256, 0, st>>>(n, grp, gci, gv, F->row_begin, bounds[q], bounds[q + 1],
+                                               roff.as<int64_t>(), sc[q].as<int32_t>(), sr[q].as<int32_t>(),
+                                               sv[q].as<double>());
+        ctx->launches += 2;
     }
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(off.p, hoff.data(), np * 8, cudaMemcpyHostToDevice, st));
-    AFSAI_CUDA_TRY(sc.alloc(std::max<int64_t>(nnz, 1) * 4, st));
-    AFSAI_CUDA_TRY(sr.alloc(std::max<int64_t>(nnz, 1) * 4, st));
-    AFSAI_CUDA_TRY(sv.alloc(std::max<int64_t>(nnz, 1) * 8, st));
-    scatter_dest_kernel<<<grid, 256, 0, st>>>(nnz, tc.as<int32_t>(), tr.as<int32_t>(), tv.as<double>(),
-                                              dbounds.as<int64_t>(), np, off.as<unsigned long long>(),
-                                              cur.as<unsigned long long>(), sc.as<int32_t>(), sr.as<int32_t>(),
-                                              sv.as<double>());
-    ctx->launches += 1;
-    // exchange counts: rcount[q] = entries q sends me
-    DevBuf scount, rcount;
-    AFSAI_CUDA_TRY(scount.alloc(np * 8, st));
-    AFSAI_CUDA_TRY(rcount.alloc(np * 8, st));
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(scount.p, hc.data(), np * 8, cudaMemcpyHostToDevice, st));
+    dt.mark("extract remote");
+    // ---- exchange counts (each rank sends to lower ranks, receives from higher ranks)
+    DevBuf dcnt;
+    AFSAI_CUDA_TRY(dcnt.alloc(2 * np * 8, st));
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(dcnt.p, scnt.data(), np * 8, cudaMemcpyHostToDevice, st));
     {
         KTimer kt(ctx, AFSAI_K_COMM);
         AFSAI_NCCL_TRY(ncclGroupStart());
-        for (int q = 0; q < np; ++q) {
-            AFSAI_NCCL_TRY(ncclSend(scount.as<int64_t>() + q, 1, ncclInt64, q, ctx->comm, st));
-            AFSAI_NCCL_TRY(ncclRecv(rcount.as<int64_t>() + q, 1, ncclInt64, q, ctx->comm, st));
-        }
+        for (int q = 0; q < me; ++q) AFSAI_NCCL_TRY(ncclSend(dcnt.as<int64_t>() + q, 1, ncclInt64, q, ctx->comm, st));
+        for (int q = me + 1; q < np; ++q)
+            AFSAI_NCCL_TRY(ncclRecv(dcnt.as<int64_t>() + np + q, 1, ncclInt64, q, ctx->comm, st));
         AFSAI_NCCL_TRY(ncclGroupEnd());
     }
-    std::vector<int64_t> hr(np);
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(hr.data(), rcount.p, np * 8, cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> rcnt(np, 0), hall(2 * np);
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(hall.data(), dcnt.p, 2 * np * 8, cudaMemcpyDeviceToHost, st));
     AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
-    int64_t total = 0;
-    std::vector<int64_t> roff(np);
-    for (int q = 0; q < np; ++q) {
-        roff[q] = total;
-        total += hr[q];
+    int64_t total_r = 0;
+    std::vector<int64_t> rbase(np, 0);
+    for (int q = me + 1; q < np; ++q) {
+        rcnt[q] = hall[np + q];
+        rbase[q] = total_r;
+        total_r += rcnt[q];
     }
     DevBuf rc_, rr_, rv_;
-    AFSAI_CUDA_TRY(rc_.alloc(std::max<int64_t>(total, 1) * 4, st));
-    AFSAI_CUDA_TRY(rr_.alloc(std::max<int64_t>(total, 1) * 4, st));
-    AFSAI_CUDA_TRY(rv_.alloc(std::max<int64_t>(total, 1) * 8, st));
+    AFSAI_CUDA_TRY(rc_.alloc(std::max<int64_t>(total_r, 1) * 4, st));
+    AFSAI_CUDA_TRY(rr_.alloc(std::max<int64_t>(total_r, 1) * 4, st));
+    AFSAI_CUDA_TRY(rv_.alloc(std::max<int64_t>(total_r, 1) * 8, st));
     {
         KTimer kt(ctx, AFSAI_K_COMM);
         AFSAI_NCCL_TRY(ncclGroupStart());
-        for (int q = 0; q < np; ++q) {
-            if (hr[q] > 0) {
-                AFSAI_NCCL_TRY(ncclRecv(rc_.as<int32_t>() + roff[q], hr[q], ncclInt32, q, ctx->comm, st));
-                AFSAI_NCCL_TRY(ncclRecv(rr_.as<int32_t>() + roff[q], hr[q], ncclInt32, q, ctx->comm, st));
-                AFSAI_NCCL_TRY(ncclRecv(rv_.as<double>() + roff[q], hr[q], ncclDouble, q, ctx->comm, st));
+        for (int q = 0; q < me; ++q)
+            if (scnt[q] > 0) {
+                AFSAI_NCCL_TRY(ncclSend(sc[q].p, scnt[q], ncclInt32, q, ctx->comm, st));
+                AFSAI_NCCL_TRY(ncclSend(sr[q].p, scnt[q], ncclInt32, q, ctx->comm, st));
+                AFSAI_NCCL_TRY(ncclSend(sv[q].p, scnt[q], ncclDouble, q, ctx->comm, st));
             }
-            if (hc[q] > 0) {
-                AFSAI_NCCL_TRY(ncclSend(sc.as<int32_t>() + hoff[q], hc[q], ncclInt32, q, ctx->comm, st));
-                AFSAI_NCCL_TRY(ncclSend(sr.as<int32_t>() + hoff[q], hc[q], ncclInt32, q, ctx->comm, st));
-                AFSAI_NCCL_TRY(ncclSend(sv.as<double>() + hoff[q], hc[q], ncclDouble, q, ctx->comm, st));
+        for (int q = me + 1; q < np; ++q)
+            if (rcnt[q] > 0) {
+                AFSAI_NCCL_TRY(ncclRecv(rc_.as<int32_t>() + rbase[q], rcnt[q], ncclInt32, q, ctx->comm, st));
+                AFSAI_NCCL_TRY(ncclRecv(rr_.as<int32_t>() + rbase[q], rcnt[q], ncclInt32, q, ctx->comm, st));
+                AFSAI_NCCL_TRY(ncclRecv(rv_.as<double>() + rbase[q], rcnt[q], ncclDouble, q, ctx->comm, st));
             }
-        }
         AFSAI_NCCL_TRY(ncclGroupEnd());
     }
-    // local G^T rows [b, e)
+    dt.mark("exchange");
+    // ---- local G^T rows [b, e): local entries + received triples
     const int64_t n_out = e - b;
-    DevBuf c2, tiles, tcol, tval;
-    AFSAI_CUDA_TRY(c2.alloc(std::max<int64_t>(n_out, 1) * 4, st));
+    DevBuf cnt, tiles, tcol, tval;
+    AFSAI_CUDA_TRY(cnt.alloc(std::max<int64_t>(n_out, 1) * 4, st));
     AFSAI_CUDA_TRY(tiles.alloc(scan_tmp_elems(n_out) * 8 + 16, st));
     AFSAI_CUDA_TRY(F->t_rowptr.alloc((n_out + 1) * 8, st));
-    AFSAI_CUDA_TRY(cudaMemsetAsync(c2.p, 0, std::max<int64_t>(n_out, 1) * 4, st));
+    AFSAI_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, std::max<int64_t>(n_out, 1) * 4, st));
     KTimer kt(ctx, AFSAI_K_TRANSPOSE);
-    count_triples_kernel<<<grid, 256, 0, st>>>(total, rc_.as<int32_t>(), b, n_out, c2.as<int32_t>());
-    ctx->launches += 1;
-    AFSAI_CUDA_TRY(exclusive_scan(c2.as<int32_t>(), n_out, F->t_rowptr.as<int64_t>(), tiles.as<int64_t>(), st,
+    count_cols_kernel<<<grid, 256, 0, st>>>(F->nnz_G, gci, b, n_out, cnt.as<int32_t>());
+    count_triples_kernel<<<grid, 256, 0, st>>>(total_r, rc_.as<int32_t>(), b, n_out, cnt.as<int32_t>());
+    ctx->launches += 2;
+    AFSAI_CUDA_TRY(exclusive_scan(cnt.as<int32_t>(), n_out, F->t_rowptr.as<int64_t>(), tiles.as<int64_t>(), st,
                                   &ctx->launches));
+    dt.mark("count+scan");
+    int64_t total = 0;
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(&total, F->t_rowptr.as<int64_t>() + n_out, 8, cudaMemcpyDeviceToHost, st));
+    AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
     F->nnz_Gt = total;
     if (F->t_col.alloc(std::max<int64_t>(total, 1) * 4, st) != cudaSuccess ||
         F->t_val.alloc(std::max<int64_t>(total, 1) * 8, st) != cudaSuccess ||
         tcol.alloc(std::max<int64_t>(total, 1) * 4, st) != cudaSuccess ||
         tval.alloc(std::max<int64_t>(total, 1) * 8, st) != cudaSuccess)
         return set_status(status, AFSAI_ENOMEM, "G^T");
-    AFSAI_CUDA_TRY(cudaMemsetAsync(c2.p, 0, std::max<int64_t>(n_out, 1) * 4, st));
-    scatter_triples_kernel<<<grid, 256, 0, st>>>(total, rc_.as<int32_t>(), rr_.as<int32_t>(), rv_.as<double>(), b,
-                                                 n_out, F->t_rowptr.as<int64_t>(), c2.as<int32_t>(),
+    AFSAI_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, std::max<int64_t>(n_out, 1) * 4, st));
+    dt.mark("alloc");
+    scatter_t_kernel<<<grid, 256, 0, st>>>(n, grp, gci, gv, F->row_begin, b, n_out, F->t_rowptr.as<int64_t>(),
+                                           cnt.as<int32_t>(), tcol.as<int32_t>(), tval.as<double>());
+    scatter_triples_kernel<<<grid, 256, 0, st>>>(total_r, rc_.as<int32_t>(), rr_.as<int32_t>(), rv_.as<double>(), b,
+                                                 n_out, F->t_rowptr.as<int64_t>(), cnt.as<int32_t>(),
                                                  tcol.as<int32_t>(), tval.as<double>());
+    dt.mark("scatter");
     sort_rows_kernel<<<grid, 256, 0, st>>>(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(),
                                            F->t_col.as<int32_t>(), F->t_val.as<double>());
-    ctx->launches += 2;
+    dt.mark("sort");
+    ctx->launches += 3;
     AFSAI_CUDA_TRY(cudaGetLastError());
     return AFSAI_OK;
 }
