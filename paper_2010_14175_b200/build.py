@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     inc, libdir = _nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
-    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "afsai.h")]
+    hdrs = (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            [os.path.join(ROOT, "include", "afsai.h")])
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
     objs, todo = [], []
     for s in srcs:

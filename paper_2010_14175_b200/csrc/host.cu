@@ -165,7 +165,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         const int h = std::atoi(e);
         if (h >= 64 && (h & (h - 1)) == 0) H = h;
     }
-    int cact = 64;
+    int cact = 56;  // active candidate slots (7-point interior rows peak near 50)
     SetupKArgs a{};
     a.rowptr = Aext.rowptr;
     a.col = Aext.col;
@@ -218,7 +218,10 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         if (rb * rpw > 200 * 1024) return set_status(status, AFSAI_ELIMIT, "a warp's rows exceed shared memory");
         // CTA size (1..8 warps) maximising the rows resident per SM
         int wpc = 1, occ = 0, best = -1;
-        for (int wc = 1; wc <= 8; ++wc) {
+        cudaFuncAttributes fa;
+        AFSAI_CUDA_TRY(cudaFuncGetAttributes(&fa, (const void *)f));
+        const int wmax = std::max(1, std::min(8, fa.maxThreadsPerBlock / 32));
+        for (int wc = 1; wc <= wmax; ++wc) {
             const size_t sm_ = (size_t)rb * wc * rpw;
             if (sm_ > 227 * 1024) break;
             if (cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_) !=

@@ -72,8 +72,10 @@ __device__ __forceinline__ int hinsert(int32_t *hkey, int H, int log2H, int32_t 
     return -1;
 }
 
-// strictly-lower packed row-major L: L[q][c], c < q, at q(q-1)/2 + c
-__device__ __forceinline__ int tri(int q) { return (q * (q - 1)) >> 1; }
+// packed row-major L: L[q][c], c < q, at q(q+1)/2 + c (the diagonal slot is
+// unused: with this offset any 16 consecutive rows start in distinct banks, so
+// a column read by 16 lanes is conflict free; q(q-1)/2 collides rows 0 and 1)
+__device__ __forceinline__ int tri(int q) { return (q * (q + 1)) >> 1; }
 
 // (|a|, ja) better than (|b|, jb)?  |acc| descending, then column ascending.
 __device__ __forceinline__ bool better(double aa, int32_t ja, double ab, int32_t jb) {
@@ -88,7 +90,7 @@ __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) { retur
 //    of column k turns its accumulator into L[q][k] = t * inv[k] and broadcasts
 //    it; every lane folds fma(-L[q][k], L[c][k], t_c) into its own columns.
 //    Accumulators of already finalized columns are dead, so the fold runs
-//    unpredicated (their loads read the zero row to stay in bounds).
+//    unpredicated (their loads read any in-bounds row: inv).
 //  - new columns (the diagonal of each new row and the couplings between new
 //    rows) are few: every lane keeps them redundantly, no broadcast needed.
 // Every accumulator folds in k-ascending order, exactly DESIGN.md C5.
@@ -118,7 +120,7 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        Lr[tt] = (c < qf) ? w.L + tri(c) : w.zero;
+        Lr[tt] = (c < qf) ? w.L + tri(c) : w.inv;  // dead columns: any in-bounds row
     }
     // ---- stages over the old columns k < qf.  The shared-memory operands of
     //      stage k+1 are loaded during stage k (software pipelining), so a stage's

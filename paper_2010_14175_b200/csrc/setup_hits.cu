@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
     unsigned long long c_steps = 0, c_border = 0, c_back = 0, c_gfma = 0;
     unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int x = gl; x <= a.mmax; x += LPR) w.zero[x] = 0.0;
     G.sync();
     long long tph = clock64();
 #define PHASE(idx)                       \

@@ -6,7 +6,7 @@
 namespace afsai {
 
 struct HitState {
-    double *inv, *y, *g, *L, *arow, *brow, *dscr, *zero, *hv, *acc;
+    double *inv, *y, *g, *L, *arow, *brow, *dscr, *hv, *acc;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey;
     int16_t *ahs, *afree;
@@ -16,7 +16,7 @@ struct HitState {
 
 template <int HC>
 __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc) {
-    int64_t dbl = 3 * (int64_t)M + (M * (M - 1)) / 2 + 1 + (int64_t)S * M + S + 2 + M + 1 + (int64_t)CA * HC +
+    int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (int64_t)CA * HC +
                   (acc ? CA : 0);
     int64_t i64 = S;
     int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA;
@@ -36,11 +36,10 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.inv = d; d += M;
     w.y = d; d += M;
     w.g = d; d += M;
-    w.L = d; d += (M * (M - 1)) / 2 + 1;
+    w.L = d; d += (M * (M + 1)) / 2 + 1;
     w.arow = d; d += S * M;
     w.brow = d; d += S;
     w.dscr = d; d += 2;
-    w.zero = d; d += M + 1;
     w.hv = d; d += CA * HC;  // [h][a]
     w.acc = nullptr;
     if (acc) { w.acc = d; d += CA; }

@@ -128,7 +128,7 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        Lr[tt] = (active && c < qf) ? w.L + tri(c) : w.zero;
+        Lr[tt] = (active && c < qf) ? w.L + tri(c) : w.inv;  // dead columns: any in-bounds row
     }
     const int qlim = (active && qf > 0) ? qf - 1 : 0;  // clamp for the operand prefetch
     double inv_n = w.inv[0], y_n = w.y[0], lsm_n[NT];
@@ -286,7 +286,10 @@ __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool
 }
 
 template <int LPR, int NT, int GS, int HC>
-__global__ void __launch_bounds__(256, 1) afsai_setup_rows_lockstep_kernel(SetupKArgs a) {
+// 16 lanes per row: <= 170 registers (three warps per SMSP register file) and CTAs
+// of up to three warps (six rows: the per-CTA shared-memory reserve then fits 18
+// rows per SM)
+__global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai_setup_rows_lockstep_kernel(SetupKArgs a) {
     extern __shared__ __align__(16) char smem[];
     constexpr int RPW = 32 / LPR;
     const int lane = threadIdx.x & 31;
@@ -297,7 +300,6 @@ __global__ void __launch_bounds__(256, 1) afsai_setup_rows_lockstep_kernel(Setup
     unsigned long long c_steps = 0, c_border = 0, c_back = 0, c_gfma = 0;
     unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int x = gl; x <= a.mmax; x += LPR) w.zero[x] = 0.0;
     G.sync();
     long long tph = clock64();
 #define PHASE(idx)                       \

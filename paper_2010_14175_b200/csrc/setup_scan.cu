@@ -31,7 +31,7 @@ namespace afsai {
 
 // On-chip state of one row (one group), carved from dynamic shared memory.
 struct RowState {
-    double *inv, *y, *g, *L, *arow, *brow, *dscr, *zero, *hacc;
+    double *inv, *y, *g, *L, *arow, *brow, *dscr, *hacc;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *selt, *glen, *misc, *coff;
     int16_t *clist, *clen;
@@ -43,7 +43,7 @@ __host__ __device__ inline int cand_cap(int H) { return (3 * H) / 4 + 8; }
 
 __host__ __device__ inline int64_t row_state_bytes(int H, int M, int S, bool hacc) {
     const int CL = cand_cap(H);
-    int64_t dbl = 3 * (int64_t)M + (M * (M - 1)) / 2 + 1 + (int64_t)S * M + S + 2 + M + 1 + (hacc ? H : 0);
+    int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (hacc ? H : 0);
     int64_t i64 = S;
     int64_t i32 = (int64_t)H + M + 3 * S + 4 + CL;
     int64_t i16 = 2 * (int64_t)CL;
@@ -61,11 +61,10 @@ __device__ __forceinline__ RowState carve(char *base, const SetupKArgs &a, bool 
     w.inv = d; d += M;
     w.y = d; d += M;
     w.g = d; d += M;
-    w.L = d; d += (M * (M - 1)) / 2 + 1;
+    w.L = d; d += (M * (M + 1)) / 2 + 1;
     w.arow = d; d += S * M;
     w.brow = d; d += S;
     w.dscr = d; d += 2;
-    w.zero = d; d += M + 1;
     w.hacc = nullptr;
     if (hacc) { w.hacc = d; d += H; }
     int64_t *l8 = reinterpret_cast<int64_t *>(d);
@@ -166,7 +165,6 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
     unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
     // per-phase SM cycles (group leader): prologue, gradient, select, gather, border, backsub, output
     long long ph[7] = {0, 0, 0, 0, 0, 0, 0};
-    for (int x = gl; x <= a.mmax; x += LPR) w.zero[x] = 0.0;
     G.sync();
     long long tph = clock64();
 #define PHASE(idx)                       \
