@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "afsai_internal.h"
 #include "assemble.h"
@@ -166,6 +167,21 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         if (h >= 64 && (h & (h - 1)) == 0) H = h;
     }
     int cact = 56;  // active candidate slots (7-point interior rows peak near 50)
+    // pattern-row kernel for long rows (FE): universe ~ (mmax+1) * len / 10 keys,
+    // table at most 3/4 full; lists hold every pattern row (no overflow)
+    // (its row descriptors hold entry offsets relative to row i as int32)
+    bool prow = !hits && prow_kernel_for(mmax, p.s, max_row_len) != nullptr && Aext.nnz < INT32_MAX;
+    if (const char *e = std::getenv("AFSAI_PROW")) prow = prow && std::atoi(e) != 0;
+    const int lcap = (int)std::min<int64_t>(1 << 15, (int64_t)(mmax + 1) * max_row_len);
+    if (prow) {
+        const int64_t u = std::max<int64_t>(48, (int64_t)(mmax + 1) * max_row_len / 10);
+        H = 1 << ilog2((int)std::min<int64_t>(1 << 14, (u * 4 + 2) / 3));
+        if (const char *e = std::getenv("AFSAI_TABLE")) {
+            const int h = std::atoi(e);
+            if (h >= 64 && (h & (h - 1)) == 0) H = h;
+        }
+        if (prow_row_bytes(H, mmax, p.s, lcap) > 200 * 1024) prow = false;
+    }
     SetupKArgs a{};
     a.rowptr = Aext.rowptr;
     a.col = Aext.col;
@@ -193,26 +209,34 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     a.retry_count = W.retry_count.as<int32_t>();
     a.work = W.work.as<unsigned long long>();
     a.counters = W.counters.as<unsigned long long>();
-    int64_t todo = nrows;
+    a.lcap = lcap;
     bool first = true;
-    DevBuf retry_in;
-    int32_t retried_total = 0;
-    while (todo > 0) {
+    // One pass of the current plan over rows (device list) or [row_lo, row_lo+n);
+    // returns the number of rows that overflowed an on-chip table in *rc.
+    auto pass = [&](const int64_t *rows, int64_t n, int32_t *rc) -> int {
         if (H > (1 << 15)) return set_status(status, AFSAI_ELIMIT, "candidate table would exceed 32768 slots");
         a.H = H;
         a.log2H = ilog2(H);
         a.cact = cact;
+        a.rows = rows;
+        a.nrows = n;
         SetupKernFn f = nullptr;
         if (hits && lockstep) {
             f = lockstep_kernel_for(ls_lpr, mmax, p.s, hc);
             if (f) lpr = ls_lpr;
+        }
+        if (!f && prow) {
+            f = prow_kernel_for(mmax, p.s, max_row_len);
+            lpr = 32;
         }
         if (!f) {
             lpr = lpr0;
             f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
         }
         if (!f) return set_status(status, AFSAI_ELIMIT, "no kernel instance for this pattern size");
-        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc) : scan_row_bytes(H, mmax, p.s);
+        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc)
+                           : prow ? prow_row_bytes(H, mmax, p.s, lcap)
+                                  : scan_row_bytes(H, mmax, p.s);
         a.warp_smem = (int32_t)rb;
         const int rpw = 32 / lpr;  // rows per warp
         if (rb * rpw > 200 * 1024) return set_status(status, AFSAI_ELIMIT, "a warp's rows exceed shared memory");
@@ -238,34 +262,76 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         AFSAI_CUDA_TRY(cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         occ = std::max(1, occ);
         int64_t grid = (int64_t)ctx->num_sms * occ;
-        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (todo + rows_per_cta - 1) / rows_per_cta));
+        grid = std::max<int64_t>(1, std::min<int64_t>(grid, (n + rows_per_cta - 1) / rows_per_cta));
         if (first) {
             stats->table_size = H;
             stats->rows_per_cta = rows_per_cta;
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
-        if (!first) {
-            a.rows = retry_in.as<int64_t>();
-            a.nrows = todo;
-        }
         {
             KTimer kt(ctx, AFSAI_K_SETUP_ROWS);
             f<<<(unsigned)grid, rows_per_cta * lpr, smem, ctx->stream>>>(a);
             AFSAI_CUDA_TRY(cudaGetLastError());
         }
         ctx->launches += 1;
-        int32_t rc = 0;
-        AFSAI_CUDA_TRY(cudaMemcpyAsync(&rc, W.retry_count.p, sizeof rc, cudaMemcpyDeviceToHost, ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(rc, W.retry_count.p, sizeof *rc, cudaMemcpyDeviceToHost, ctx->stream));
         AFSAI_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        return AFSAI_OK;
+    };
+    // Table-size probe for the hit-list plans: the stencil's universe depends on
+    // the coefficients (anisotropy spreads the pattern), so a strided sample of
+    // rows is run first; while more than 1% of it overflows, table and active
+    // candidate slots double (the sample's results are recomputed by the main pass).
+    const bool probe_env = std::getenv("AFSAI_TABLE") == nullptr && std::getenv("AFSAI_NOPROBE") == nullptr;
+    if (hits && probe_env && nrows >= 32768) {
+        const int64_t ns = 2048, stride = nrows / ns;
+        std::vector<int64_t> hs((size_t)ns);
+        for (int64_t t = 0; t < ns; ++t) hs[(size_t)t] = row_lo + t * stride;
+        DevBuf sample;
+        AFSAI_CUDA_TRY(sample.alloc(ns * sizeof(int64_t), ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(sample.p, hs.data(), ns * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        for (int it = 0; it < 3; ++it) {
+            int32_t rc = 0;
+            const int r = pass(sample.as<int64_t>(), ns, &rc);
+            if (r != AFSAI_OK) return r;
+            first = false;
+            if (rc * 100 <= ns) break;
+            if (hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 > 200 * 1024) break;
+            H *= 2;
+            cact *= 2;
+        }
+        AFSAI_CUDA_TRY(cudaMemsetAsync(W.counters.p, 0, 32 * sizeof(unsigned long long), ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemsetAsync(W.err.p, 0xff, sizeof(unsigned long long), ctx->stream));
+        first = true;
+    }
+    int64_t todo = nrows;
+    DevBuf retry_in;
+    int32_t retried_total = 0;
+    const int64_t *rows = nullptr;
+    while (todo > 0) {
+        int32_t rc = 0;
+        const int r = pass(rows, todo, &rc);
+        if (r != AFSAI_OK) return r;
         todo = rc;
         if (rc > 0) {
             retried_total += rc;
             AFSAI_CUDA_TRY(retry_in.alloc(rc * sizeof(int64_t), ctx->stream));
             AFSAI_CUDA_TRY(cudaMemcpyAsync(retry_in.p, W.retry.p, rc * sizeof(int64_t), cudaMemcpyDeviceToDevice,
                                            ctx->stream));
-            H *= 4;
-            hits = false;  // retries use the general kernel
+            rows = retry_in.as<int64_t>();
+            if (prow && prow_row_bytes(2 * H, mmax, p.s, lcap) <= 200 * 1024) {
+                H *= 2;  // pattern-row kernel with a larger table
+            } else if (hits && lockstep && hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 <= 200 * 1024) {
+                H *= 2;  // hit-list kernel with a larger table and more candidate slots
+                cact *= 2;
+            } else {
+                if (prow) H = 1 << std::max(6, ilog2((int)std::min<int64_t>(
+                                  1 << 13, std::max<int64_t>(4 * (mmax + 1), (int64_t)(mmax + 1) * max_row_len / 6))));
+                prow = false;
+                H *= 4;
+                hits = false;  // retries use the general kernel
+            }
         }
         first = false;
     }

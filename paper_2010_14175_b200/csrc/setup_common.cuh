@@ -155,11 +155,11 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
             double l[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
-            if (gl == ln) {
+            // broadcast values: every lane stores the same bits (no divergent branch
+            // before the next stage's shuffles)
 #pragma unroll
-                for (int u = 0; u < GS; ++u)
-                    if (u < gs) Lnew[u][k] = l[u];
-            }
+            for (int u = 0; u < GS; ++u)
+                if (u < gs) Lnew[u][k] = l[u];
 #pragma unroll
             for (int t2 = 0; t2 < NT; ++t2)
 #pragma unroll
@@ -186,17 +186,15 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
         const double inv_k = 1.0 / dq;
         const double y_k = ty[uf] * inv_k;
         psi = fma(-y_k, y_k, psi);     // C6
-        if (gl == 0) {
-            w.inv[k] = inv_k;
-            w.y[k] = y_k;
-        }
+        w.inv[k] = inv_k;  // redundant values: every lane stores the same bits
+        w.y[k] = y_k;
         double lu[GS];
 #pragma unroll
         for (int u = 0; u < GS; ++u) {
             lu[u] = 0.0;
             if (u > uf && u < gs) {
                 lu[u] = cp[u][uf] * inv_k;
-                if (gl == 0) Lnew[u][k] = lu[u];
+                Lnew[u][k] = lu[u];
             }
         }
 #pragma unroll
@@ -261,7 +259,7 @@ __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
                 }
             }
             const double gk = G.bcast(tb[tt] * iv, ln);
-            if (gl == ln) w.g[k] = gk;
+            w.g[k] = gk;  // broadcast value, stored by every lane
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
         }

@@ -20,6 +20,7 @@ struct SetupKArgs {
     double eps;
     int32_t H, log2H;   // per-row hash table slots (power of two)
     int32_t cact;       // hit-list kernel: active candidate slots per row
+    int32_t lcap;       // pattern-row kernel: list entries per row
     int32_t warp_smem;  // bytes of shared memory per row (group)
     // outputs, index = global row - out_base
     int64_t out_base;
@@ -46,5 +47,8 @@ SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);
 int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);
 // hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4, mmax <= 6*lpr)
 SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);
+// pattern-row kernel (long rows, s <= 4, mmax <= 128, rows <= 128 entries): 32 lanes per row
+SetupKernFn prow_kernel_for(int mmax, int s, int64_t max_row_len);
+int64_t prow_row_bytes(int H, int mmax, int s, int lcap);
 
 }  // namespace afsai

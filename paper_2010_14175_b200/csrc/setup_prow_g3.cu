@@ -1,0 +1,6 @@
+// setup_prow_g3.cu -- pattern-row set-up kernel instances with 3 new columns bordered in lockstep.
+#include "setup_prow_impl.cuh"
+
+namespace afsai {
+template SetupKernFn prow_instance<3>(int nt, int nv);
+}  // namespace afsai

@@ -34,7 +34,7 @@ for r in range(reps):
 out["wall_ms"] = (t1 - t0) * 1e3
 out.update({k_: st[k_] for k_ in ["ms_total", "ms_rows", "ms_assemble", "ms_transpose", "nnz_G", "table_size",
                                    "rows_per_cta", "retried_rows", "fma_border", "fma_backsub", "fma_grad",
-                                   "grad_entries", "steps_total", "rows_by_reason"]})
+                                   "grad_entries", "steps_total", "rows_by_reason", "max_universe"]})
 ph = st["phase_cycles"]
 names = ["prologue", "gradient", "select", "gather", "border", "backsub", "output"]
 tot = sum(ph)

@@ -74,6 +74,11 @@ CASES = [
     ("dense90_s16", lambda: ai.from_dense(ai.random_spd_dense(90, sub=90)), 8, 16, 0.0, 1 << 30),
     ("dense130_cap129", lambda: ai.from_dense(ai.random_spd_dense(130, sub=130)), 200, 1, 0.0, 129),
     ("single_row", lambda: ai.diagonal([3.0]), 5, 2, 0.0, 1 << 30),
+    # pattern-row kernel instances (long rows, s <= 4) and the hit-list table probe
+    ("fe_4_12x1", lambda: ai.fe_elasticity(4), 12, 1, 0.0, 100),
+    ("fe_4_10x2_cap15", lambda: ai.fe_elasticity(4), 10, 2, 0.0, 15),
+    ("rsparse_s4", lambda: ai.random_sparse_spd(3000, 10, sub=6), 8, 4, 0.0, 1 << 30),
+    ("hetero_32_probe", lambda: ai.hetero_poisson3d(32), 20, 2, 0.0, 1 << 30),
 ]
 
 
@@ -101,6 +106,28 @@ def test_setup_parity(ctx, name, make, k, s, eps, cap):
     assert np.array_equal(T.rowptr, Tr.rowptr) and np.array_equal(T.col, Tr.col)
     assert np.array_equal(T.val.view(np.int64), Tr.val.view(np.int64))
     F.close()
+
+
+@pytest.mark.parametrize("env", [{"AFSAI_TABLE": "64"}, {"AFSAI_PROW": "0"}, {"AFSAI_NOPROBE": "1"}],
+                         ids=["prow_retry_from_64", "scan_kernel", "hits_no_probe"])
+def test_setup_parity_plans(ctx, env, monkeypatch):
+    """The other kernel plans (forced small tables and retries, the general scan
+    kernel on FE rows, the hit-list kernel without the table probe) give the
+    same bits as the oracle."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    cases = [(ai.fe_elasticity(4), 30, 3, 100)]
+    if "AFSAI_NOPROBE" in env:
+        cases = [(ai.hetero_poisson3d(32), 20, 2, 1 << 30)]
+    for A, k, s, cap in cases:
+        F = gpu_setup(ctx, A, k, s, 0.0, cap)
+        G = host_csr(F)
+        ref = oracle.setup(A, k, s, 0.0, cap)
+        flagged, nonbit = compare_rows(G, ref, np.arange(A.n), str(env))
+        assert not flagged and nonbit == 0
+        if "AFSAI_TABLE" in env:
+            assert F.stats()["retried_rows"] > 0
+        F.close()
 
 
 def apply_tolerance(G, Gt, r):
