@@ -231,6 +231,15 @@ def fe_elasticity(N: int, nu: float = 0.3, hetero: bool = True) -> CSR:
     N x N x N free nodes (the z = 0 plane is clamped and eliminated), 3 dof/node,
     node-major, x fastest; per-element log10 E ~ U(-1, 1).  Couplings summed in
     ascending element order, then the strictly-upper part is mirrored from the lower."""
+    return fe_elasticity_rows(N, 0, 3 * N * N * N, nu, hetero)
+
+
+def fe_elasticity_rows(N: int, row_lo: int, row_hi: int, nu: float = 0.3, hetero: bool = True) -> CSR:
+    """Rows [row_lo, row_hi) of fe_elasticity(N), bitwise identical to the full
+    matrix's rows (every node's couplings depend only on its own coordinates and the
+    global element moduli; the mirror needs the blocks of nodes one plane away).
+    Returned as a CSR with n = row_hi - row_lo rows, GLOBAL column indices, and
+    attribute n_cols = 3 N^3 (multi-GPU slabs without building the whole matrix)."""
     Ke = _q1_hex_stiffness(nu)
     ne_x = N - 1
     ne_z = N
@@ -239,8 +248,12 @@ def fe_elasticity(N: int, nu: float = 0.3, hetero: bool = True) -> CSR:
         E = 10.0 ** rng("fe_E").uniform(-1.0, 1.0, n_el)
     else:
         E = np.ones(n_el)
-    nn = N * N * N
-    a = np.arange(nn, dtype=np.int64)
+    nn_all = N * N * N
+    node_lo, node_hi = row_lo // 3, -(-row_hi // 3)
+    halo = N * N + N + 1
+    g_lo, g_hi = max(0, node_lo - halo), min(nn_all, node_hi + halo)
+    a = np.arange(g_lo, g_hi, dtype=np.int64)   # computed nodes (slab + mirror halo)
+    nn = len(a)
     ax, ay, az = a % N, (a // N) % N, a // (N * N) + 1   # az: physical plane index 1..N
     offsets = [(dx, dy, dz) for dz in (-1, 0, 1) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
     dindex = {d: k for k, d in enumerate(offsets)}
@@ -261,28 +274,35 @@ def fe_elasticity(N: int, nu: float = 0.3, hetero: bool = True) -> CSR:
             contrib = np.where(okb[:, None, None], Ee[:, None, None] * blk[None], 0.0)
             k = dindex[d]
             blocks[:, k] = blocks[:, k] + contrib
-    # neighbour validity (node b exists and is free)
-    valid = np.zeros((nn, 27), dtype=bool)
-    bidx = np.zeros((nn, 27), dtype=np.int64)
+    # neighbour validity (node b exists and is free), for the slab nodes only
+    s0, s1 = node_lo - g_lo, node_hi - g_lo
+    asl = a[s0:s1]
+    sx, sy, sz = ax[s0:s1], ay[s0:s1], az[s0:s1]
+    ns = len(asl)
+    valid = np.zeros((ns, 27), dtype=bool)
+    bidx = np.zeros((ns, 27), dtype=np.int64)
     for k, (dx, dy, dz) in enumerate(offsets):
-        bx, by, bz = ax + dx, ay + dy, az + dz
+        bx, by, bz = sx + dx, sy + dy, sz + dz
         v = (bx >= 0) & (bx < N) & (by >= 0) & (by < N) & (bz >= 1) & (bz <= N)
         valid[:, k] = v
-        bidx[:, k] = np.where(v, bx + N * (by + N * (bz - 1)), 0)
+        bidx[:, k] = np.where(v, bx + N * (by + N * (bz - 1)), g_lo)
     # mirror: upper entries (3b+j > 3a+i) := lower entries of the transposed block
-    rows_g = 3 * a[:, None, None, None] + np.arange(3)[None, None, :, None]
+    rows_g = 3 * asl[:, None, None, None] + np.arange(3)[None, None, :, None]
     cols_g = 3 * bidx[:, :, None, None] + np.arange(3)[None, None, None, :]
     upper = (cols_g > rows_g) & valid[:, :, None, None]
     opp = np.array([dindex[(-dx, -dy, -dz)] for (dx, dy, dz) in offsets])
-    mirrored = blocks[bidx, opp[None, :]]            # (nn, 27, 3, 3) block of (b, -d)
+    mirrored = blocks[bidx - g_lo, opp[None, :]]     # (ns, 27, 3, 3) block of (b, -d)
     mirrored = np.swapaxes(mirrored, 2, 3)
-    blocks = np.where(upper, mirrored, blocks)
+    blocks = np.where(upper, mirrored, blocks[s0:s1])
     del mirrored, upper
     # rows 3a+i: columns over d ascending (== b ascending), then j
-    vals = np.transpose(blocks, (0, 2, 1, 3)).reshape(nn * 3, 81)
-    cols = np.transpose(np.broadcast_to(cols_g, (nn, 27, 3, 3)), (0, 2, 1, 3)).reshape(nn * 3, 81)
-    vmask = np.broadcast_to(valid[:, None, :, None], (nn, 3, 27, 3)).reshape(nn * 3, 81)
-    return _from_row_blocks(3 * nn, cols, vals, vmask, f"fe_{N}")
+    vals = np.transpose(blocks, (0, 2, 1, 3)).reshape(ns * 3, 81)
+    cols = np.transpose(np.broadcast_to(cols_g, (ns, 27, 3, 3)), (0, 2, 1, 3)).reshape(ns * 3, 81)
+    vmask = np.broadcast_to(valid[:, None, :, None], (ns, 3, 27, 3)).reshape(ns * 3, 81)
+    r0, r1 = row_lo - 3 * node_lo, row_hi - 3 * node_lo
+    out = _from_row_blocks(r1 - r0, cols[r0:r1], vals[r0:r1], vmask[r0:r1], f"fe_{N}")
+    out.n_cols = 3 * nn_all
+    return out
 
 
 # ---------------------------------------------------------------- random SPD (tests)

@@ -16,6 +16,10 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "build_obj")
 LIB = os.path.join(LIBDIR, "libafsai_b200.so")
+# --debug: bounds-checked variant (AFSAI_BOUNDS_CHECK: every row-pointer lookup of
+# the set-up kernels traps with the offending index), loaded when AFSAI_DEBUG_LIB=1
+OBJDIR_DBG = os.path.join(HERE, "build_obj_dbg")
+LIB_DBG = os.path.join(LIBDIR, "libafsai_b200_dbg.so")
 ROOT = os.path.dirname(HERE)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,9 +46,12 @@ def _flags_for(src: str):
     return flags
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    objdir = OBJDIR_DBG if debug else OBJDIR
+    lib_out = LIB_DBG if debug else LIB
+    extra = ["-DAFSAI_BOUNDS_CHECK"] if debug else []
     os.makedirs(LIBDIR, exist_ok=True)
-    os.makedirs(OBJDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     inc, libdir = _nccl_dirs()
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
@@ -52,16 +59,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
     objs, todo = [], []
     for s in srcs:
-        o = os.path.join(OBJDIR, os.path.basename(s) + ".o")
+        o = os.path.join(objdir, os.path.basename(s) + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
             todo.append((s, o))
 
     def compile_one(so):
         s, o = so
-        cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s)
+        cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s) + extra
         r = subprocess.run(cmd, capture_output=True, text=True)
-        with open(os.path.join(OBJDIR, os.path.basename(s) + ".ptxas.txt"), "w") as f:
+        with open(os.path.join(objdir, os.path.basename(s) + ".ptxas.txt"), "w") as f:
             f.write(r.stderr)
         return s, r
 
@@ -73,15 +80,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"nvcc failed on {s}")
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, "-shared", "-o", LIB] + objs + ARCH + [
+    if force or not os.path.exists(lib_out) or os.path.getmtime(lib_out) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, "-shared", "-o", lib_out] + objs + ARCH + [
             "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath={libdir}", "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

@@ -34,7 +34,8 @@ int set_status(afsai_status_t *st, int code, const std::string &msg, int64_t row
         cudaError_t _e = (expr);                                                                    \
         if (_e != cudaSuccess)                                                                      \
             return ::afsai::set_status(status, AFSAI_ECUDA,                                         \
-                                       std::string(#expr " failed: ") + cudaGetErrorString(_e));    \
+                                       std::string(#expr " failed at ") + __FILE__ ":" +             \
+                                           std::to_string(__LINE__) + ": " + cudaGetErrorString(_e));  \
     } while (0)
 
 #define AFSAI_NCCL_TRY(expr)                                                                        \

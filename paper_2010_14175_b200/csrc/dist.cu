@@ -444,6 +444,17 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
     DeviceCsr X;
     rc = gather_halo(ctx, A, D->bounds, lo, &X, status);
     if (rc) return fail(rc);
+#ifdef AFSAI_BOUNDS_CHECK
+    {   // debug build: the gathered halo-extended matrix must be a valid CSR
+        int64_t ml = 0;
+        rc = validate_csr(ctx, X, &ml, status);
+        if (rc) {
+            std::fprintf(stderr, "[afsai rank %d] halo-extended A invalid: %s\n", ctx->rank,
+                         status ? status->msg : "?");
+            return fail(rc);
+        }
+    }
+#endif
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
     F->stats.halo_rows = (int32_t)(b - lo);
     rc = block_rows_to_G(ctx, X, lo, e, b, A.n_rows, p, maxlen, F, status);

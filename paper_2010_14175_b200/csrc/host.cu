@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -167,6 +168,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         if (h >= 64 && (h & (h - 1)) == 0) H = h;
     }
     int cact = 56;  // active candidate slots (7-point interior rows peak near 50)
+    // the hit-list kernels encode active slot aa as int8 state -2 - aa
+    constexpr int kMaxCact = 126;
     // pattern-row kernel for long rows (FE): universe ~ (mmax+1) * len / 10 keys,
     // table at most 3/4 full; lists hold every pattern row (no overflow)
     // (its row descriptors hold entry offsets relative to row i as int32)
@@ -187,6 +190,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     a.col = Aext.col;
     a.val = Aext.val;
     a.base = Aext.base;
+    a.nnz = Aext.nnz;
     a.a_lo = a_lo;
     a.a_hi = a_hi;
     a.rows = nullptr;
@@ -269,6 +273,13 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
+        if (std::getenv("AFSAI_DEBUG_PLAN"))
+            std::fprintf(stderr,
+                         "[afsai rank %d] pass: kernel=%s rows=%lld list=%d H=%d cact=%d lpr=%d rb=%lld "
+                         "rows/cta=%d grid=%lld a_lo=%lld a_hi=%lld row_lo=%lld base=%lld\n",
+                         ctx->rank, (hits && lockstep) ? "lockstep" : prow ? "prow" : hits ? "hits" : "scan",
+                         (long long)n, rows != nullptr, H, cact, lpr, (long long)rb, rows_per_cta, (long long)grid,
+                         (long long)a.a_lo, (long long)a.a_hi, (long long)a.row_lo, (long long)a.base);
         {
             KTimer kt(ctx, AFSAI_K_SETUP_ROWS);
             f<<<(unsigned)grid, rows_per_cta * lpr, smem, ctx->stream>>>(a);
@@ -297,7 +308,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             if (r != AFSAI_OK) return r;
             first = false;
             if (rc * 100 <= ns) break;
-            if (hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 > 200 * 1024) break;
+            if (2 * cact > kMaxCact || hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 > 200 * 1024) break;
             H *= 2;
             cact *= 2;
         }
@@ -322,7 +333,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             rows = retry_in.as<int64_t>();
             if (prow && prow_row_bytes(2 * H, mmax, p.s, lcap) <= 200 * 1024) {
                 H *= 2;  // pattern-row kernel with a larger table
-            } else if (hits && lockstep && hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 <= 200 * 1024) {
+            } else if (hits && lockstep && 2 * cact <= kMaxCact &&
+                       hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 <= 200 * 1024) {
                 H *= 2;  // hit-list kernel with a larger table and more candidate slots
                 cact *= 2;
             } else {
@@ -366,7 +378,7 @@ static int ctx_init(afsai_ctx_t c, void *stream, afsai_status_t *status) {
     // keep freed stream-ordered allocations cached in the device pool: the set-up
     // scratch and G are re-allocated every call and remapping them costs ms
     cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+    if (std::getenv("AFSAI_POOL_KEEP0") == nullptr && cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "afsai_internal.h"
@@ -82,7 +83,24 @@ __device__ __forceinline__ bool better(double aa, int32_t ja, double ab, int32_t
     return (aa > ab) || (aa == ab && ja < jb);
 }
 
-__device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) { return a.rowptr[r - a.a_lo] - a.base; }
+__device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {
+#ifdef AFSAI_BOUNDS_CHECK
+    if (r < a.a_lo || r > a.a_hi) {
+        printf("afsai bounds: row pointer of row %lld outside [%lld, %lld] (block %d thread %d)\n", (long long)r,
+               (long long)a.a_lo, (long long)a.a_hi, (int)blockIdx.x, (int)threadIdx.x);
+        return 0;  // report and continue (a trap can lose the printf buffer)
+    }
+    const int64_t v = a.rowptr[r - a.a_lo] - a.base;
+    if (v < 0 || v > a.nnz) {
+        printf("afsai bounds: row %lld starts at entry %lld outside [0, %lld]\n", (long long)r, (long long)v,
+               (long long)a.nnz);
+        return 0;
+    }
+    return v;
+#else
+    return a.rowptr[r - a.a_lo] - a.base;
+#endif
+}
 
 // Bordered Cholesky of the group of new rows q = qf .. qf+gs-1 (gathered rows in
 // arow/brow slots ug .. ug+gs-1), forward solve and psi update.

@@ -39,9 +39,9 @@ __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int
                 const int st = w.hval[sl];
                 if (st >= 0) {
                     if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
-                } else {
+                } else if (st <= -2) {
                     hit_insert<HC>(w, -2 - st, q, r, v);     // existing candidate: new hit
-                }
+                }                                            // st == -1: dropped (row overflowed)
             }
         }
     }
@@ -54,7 +54,8 @@ __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int
             const int rk = __popc(bal & ((1u << G.gl) - 1u));
             const int aa = rk < nf ? w.afree[nf - 1 - rk] : hw + (rk - nf);
             if (aa >= CA) {
-                w.misc[1] = 1;
+                w.misc[1] = 1;          // the row is retried with larger tables;
+                w.hval[sl] = (int8_t)-1;  // the key must not decode as an active slot
             } else {
                 w.hval[sl] = (int8_t)(-2 - aa);
                 w.akey[aa] = c;
@@ -105,7 +106,10 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
         const int64_t orow = i64 - a.out_base;
         const int64_t e0i = rp_of(a, i64), e1i = rp_of(a, i64 + 1);
         tph = clock64();
-        for (int sl = gl; sl < H; sl += LPR) w.hkey[sl] = kEmpty;
+        for (int sl = gl; sl < H; sl += LPR) {
+            w.hkey[sl] = kEmpty;
+            w.hval[sl] = (int8_t)-1;  // no stale shared memory is ever decoded
+        }
         for (int x = gl; x < CA; x += LPR) w.ahn[x] = 0;
         if (gl == 0) {
             w.misc[0] = 0;

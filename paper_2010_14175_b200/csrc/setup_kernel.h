@@ -12,6 +12,7 @@ struct SetupKArgs {
     const int32_t *col;
     const double *val;
     int64_t base, a_lo, a_hi;
+    int64_t nnz;  // entries of A_ext (bounds checks of the debug build)
     // rows to compute: rows ? rows[t] : row_lo + t, for t < nrows
     const int64_t *rows;
     int64_t row_lo, nrows;

@@ -49,32 +49,30 @@ __device__ __forceinline__ int hinsert_warp(int32_t *hkey, int H, int log2H, boo
 template <int NV>
 struct PRowFetch {
     double v[NV];
-    int32_t s[NV];
+    double *s[NV];  // &acc[slot]
     double gq;
 };
 
 // One pattern row from its descriptor pd[idx] = {first entry - e0i, list offset,
 // (count << 16) | position q, column}; the rows are kept in ascending column
 // order with row i (position M, g~_i = g[M] = 1) last.
+// Branch-free: rows past m read row m's descriptor with no entries.  Lanes
+// without an entry fold 0 into the spare slot acc[H].
 template <int LPR, int NV>
-__device__ __forceinline__ void prow_fetch(const PRowState &w, const SetupKArgs &a, int64_t e0i, int idx, int m,
+__device__ __forceinline__ void prow_fetch(const PRowState &w, const double *vrow, double *spare, int idx, int m,
                                            int gl, PRowFetch<NV> &f) {
-    if (idx <= m) {
-        const int4 d = w.pd[idx];
-        const int q = d.z & 0xffff, n = d.z >> 16;
-        f.gq = w.g[q];
-        const double *vb = a.val + e0i + d.x;
+    const bool live = idx <= m;
+    const int4 d = w.pd[live ? idx : m];
+    const int q = d.z & 0xffff, n = live ? (d.z >> 16) : 0;
+    f.gq = w.g[q];
+    const double *vb = vrow + d.x;
+    const int16_t *lb = w.lu + d.y;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int x = gl + LPR * v;
-            const bool in = x < n;
-            f.s[v] = in ? (int32_t)w.lu[d.y + x] : a.H;
-            f.v[v] = in ? __ldg(vb + x) : 0.0;
-        }
-    } else {
-        f.gq = 0.0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) { f.s[v] = a.H; f.v[v] = 0.0; }
+    for (int v = 0; v < NV; ++v) {
+        const int x = gl + LPR * v;
+        const bool in = x < n;
+        f.s[v] = in ? w.acc + lb[x] : spare;
+        f.v[v] = in ? __ldg(vb + x) : 0.0;
     }
 }
 
@@ -168,7 +166,10 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             {
                 PRowFetch<NV> pf[kProwDepth];
 #pragma unroll
-                for (int d = 0; d < kProwDepth; ++d) prow_fetch<LPR, NV>(w, a, e0i, d, m, gl, pf[d]);
+                const double *vrow = a.val + e0i;
+                double *const spare = w.acc + H;
+#pragma unroll
+                for (int d = 0; d < kProwDepth; ++d) prow_fetch<LPR, NV>(w, vrow, spare, d, m, gl, pf[d]);
                 for (int base = 0; base <= m; base += kProwDepth) {
 #pragma unroll
                     for (int d = 0; d < kProwDepth; ++d) {
@@ -179,13 +180,13 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                             // stores (one LDS -> DFMA -> STS chain per row).
                             double av[NV];
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) av[v] = w.acc[pf[d].s[v]];
+                            for (int v = 0; v < NV; ++v) av[v] = *pf[d].s[v];
 #pragma unroll
                             for (int v = 0; v < NV; ++v) av[v] = fma(pf[d].v[v], pf[d].gq, av[v]);
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) w.acc[pf[d].s[v]] = av[v];
+                            for (int v = 0; v < NV; ++v) *pf[d].s[v] = av[v];
                             G.sync();
-                            prow_fetch<LPR, NV>(w, a, e0i, base + d + kProwDepth, m, gl, pf[d]);
+                            prow_fetch<LPR, NV>(w, vrow, spare, base + d + kProwDepth, m, gl, pf[d]);
                         }
                     }
                 }
@@ -368,12 +369,17 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                         if (ok) w.lu[lo_u + oo[b]] = (int16_t)sl;
                         const int st = ok ? (int)w.hval[sl] : -1;
                         if (st >= 0 && st <= m + u) w.arow[u * M + st] = vv[b];
-                        nins += __popc(__ballot_sync(0xffffffffu, ins));
-                        full |= __any_sync(0xffffffffu, low && sl < 0);
+                        // lane-local counts, reduced once after the gather
+                        nins += ins;
+                        full |= low && sl < 0;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) nlow[q] += __popc(__ballot_sync(0xffffffffu, ok && u == q));
+                        for (int q = 0; q < 4; ++q) nlow[q] += (ok && u == q);
                     }
                 }
+                nins = G.sum(nins);
+                full = __any_sync(0xffffffffu, full);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) nlow[q] = q < nsel ? G.sum(nlow[q]) : 0;
                 if (gl == 0) {
                     w.misc[0] += nins;
                     if (full) w.misc[1] = 1;

@@ -102,7 +102,11 @@ __device__ __forceinline__ int universe_insert(const RowState &w, const SetupKAr
         w.misc[1] = 1;
         return -1;
     }
-    const int64_t e0 = rp_of(a, c), e1 = rp_of(a, (int64_t)c + 1);
+    // Columns below the exact halo (a_lo) are kmax+1 hops from i: they enter the
+    // universe only at the last step's gather and are never evaluated, so they get
+    // an empty extent instead of a rowptr read outside the halo.
+    const bool inside = c >= a.a_lo;
+    const int64_t e0 = inside ? rp_of(a, c) : e0i, e1 = inside ? rp_of(a, (int64_t)c + 1) : e0i;
     w.clist[p] = (int16_t)sl;
     w.coff[p] = (int32_t)(e0 - e0i);
     w.clen[p] = (int16_t)(e1 - e0);

@@ -238,12 +238,16 @@ def test_determinism_repeat(ctx):
 @pytest.mark.parametrize("make,k,s,cap", [(lambda: ai.hetero_poisson3d(12), 8, 2, 1 << 30),
                                           (lambda: ai.fe_elasticity(6), 10, 3, 100),
                                           (lambda: ai.poisson3d(14), 20, 2, 1 << 30)])
-def test_block_setup_partition_emulation(ctx, make, k, s, cap):
+@pytest.mark.parametrize("env", [{}, {"AFSAI_PROW": "0", "AFSAI_HITS": "0"}], ids=["default", "scan_kernel"])
+def test_block_setup_partition_emulation(ctx, make, k, s, cap, env, monkeypatch):
     """Rows of a block computed from a halo-extended copy of A (rows [b - k*beta, e)
     only) are bitwise the same rows of the whole-matrix set-up (pin P12 on the GPU:
-    the multi-GPU set-up's building block)."""
+    the multi-GPU set-up's building block).  Also with the general
+    scan kernel, whose last-step universe reaches one hop past the halo."""
     from paper_2010_14175_b200 import capi
     from paper_2010_14175_b200.api import DeviceCSR
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
     A = make()
     F = gpu_setup(ctx, A, k, s, 0.0, cap)
     G = host_csr(F)

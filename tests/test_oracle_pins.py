@@ -401,3 +401,18 @@ def test_generators_are_bitwise_symmetric_spd():
     assert A.nnz == 7 * 125 - 6 * 25 and A.n == 125
     A = ai.fe_elasticity(4)
     assert A.n == 3 * 64
+
+
+def test_fe_row_slabs_are_rows_of_the_full_matrix():
+    """fe_elasticity_rows (multi-GPU slabs without the whole matrix) returns exactly
+    the full generator's rows, bitwise, also for slabs that split a node's 3 rows."""
+    N = 6
+    A = ai.fe_elasticity(N)
+    n = A.n
+    for lo, hi in [(0, n), (0, 7), (5, n), (n // 3 + 1, 2 * n // 3 - 1), (n - 4, n)]:
+        S = ai.fe_elasticity_rows(N, lo, hi)
+        a, b = A.rowptr[lo], A.rowptr[hi]
+        assert S.n == hi - lo and S.n_cols == n
+        assert np.array_equal(S.rowptr, A.rowptr[lo:hi + 1] - a)
+        assert np.array_equal(S.col, A.col[a:b])
+        assert np.array_equal(S.val.view(np.int64), A.val[a:b].view(np.int64))
