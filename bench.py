@@ -267,8 +267,15 @@ def main():
     solve_kernels_ms = (ms_G + ms_T + ktimes["spmv_A"][1] + ktimes["vector"][1]) / args.steps
     if setup_ms >= max(ms_G, ms_T) / args.steps:
         achieved = setup_flop / (setup_ms * 1e-3) / 1e12
-        roof = {"kernel": "afsai_setup_rows_kernel", "bound": "alu", "achieved": achieved, "peak": fp64_peak_tf,
-                "unit": "TFLOP/s", "frac": achieved / fp64_peak_tf, "traffic": None,
+        # DRAM bytes per launch of this kernel from the committed ncu --set full capture
+        traffic = None
+        try:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_setup_traffic.json")))["dram_bytes_per_launch"]
+        except Exception:
+            pass
+        roof = {"kernel": "afsai_setup_rows_lockstep_kernel<16, 3, 2, 6>", "bound": "alu", "achieved": achieved,
+                "peak": fp64_peak_tf, "unit": "TFLOP/s", "frac": achieved / fp64_peak_tf, "traffic": traffic,
+                "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r01_setup_traffic.json)",
                 "peak_source": f"{nsm} SM x 64 DFMA/clk x 2 x {sm_max:.0f} MHz (unit counts, DESIGN.md §5)",
                 "algorithmic_flop_per_launch": setup_flop, "avg_launch_ms": setup_ms}
     else:

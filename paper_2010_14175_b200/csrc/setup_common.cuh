@@ -168,7 +168,7 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
                 inv_n = w.inv[kn];
                 y_n = w.y[kn];
 #pragma unroll
-                for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];
+                for (int t2 = tt; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];  // chunks < tt are dead
             }
             double l[GS];
 #pragma unroll
@@ -179,7 +179,7 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
             for (int u = 0; u < GS; ++u)
                 if (u < gs) Lnew[u][k] = l[u];
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2)
+            for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
                 for (int u = 0; u < GS; ++u) t[u][t2] = fma(-l[u], lsm[t2], t[u][t2]);
 #pragma unroll
@@ -271,7 +271,7 @@ __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
                 const double *Lk = w.L + tri(kn);
                 iv_n = w.inv[kn];
 #pragma unroll
-                for (int t2 = 0; t2 < NT; ++t2) {
+                for (int t2 = 0; t2 <= tt; ++t2) {  // chunks > tt are final
                     const int c = gl + LPR * t2;
                     lk_n[t2] = Lk[c < kn ? c : 0];
                 }

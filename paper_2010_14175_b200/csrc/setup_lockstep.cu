@@ -152,12 +152,12 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
                 inv_n = w.inv[kn];
                 y_n = w.y[kn];
 #pragma unroll
-                for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];
+                for (int t2 = tt; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];  // chunks < tt are dead
             }
             double l[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
-            if (live && gl == ln) {
+            if (live) {  // broadcast value: every lane of the row stores the same bits
 #pragma unroll
                 for (int u = 0; u < GS; ++u)
                     if (u < gs) Lnew[u][k] = l[u];
@@ -165,21 +165,19 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
             // t accumulators outside a row's live stages are dead (finalized old
             // columns, or columns that are not old): updated unpredicated
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2)
+            for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
                 for (int u = 0; u < GS; ++u) t[u][t2] = fma(-l[u], lsm[t2], t[u][t2]);
+            // live-stage updates as predicated fmas (no selects; signed zeros kept)
+            if (live) {
 #pragma unroll
-            for (int u = 0; u < GS; ++u) {
-                const double nd = fma(-l[u], l[u], dg[u]);
-                const double ny = fma(-l[u], y_k, ty[u]);
-                dg[u] = live ? nd : dg[u];
-                ty[u] = live ? ny : ty[u];
+                for (int u = 0; u < GS; ++u) {
+                    dg[u] = fma(-l[u], l[u], dg[u]);
+                    ty[u] = fma(-l[u], y_k, ty[u]);
 #pragma unroll
-                for (int v = 0; v < GS; ++v)
-                    if (v < u) {
-                        const double nc = fma(-l[u], l[v], cp[u][v]);
-                        cp[u][v] = live ? nc : cp[u][v];
-                    }
+                    for (int v = 0; v < GS; ++v)
+                        if (v < u) cp[u][v] = fma(-l[u], l[v], cp[u][v]);
+                }
             }
         }
     }
@@ -269,17 +267,16 @@ __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool
                 const double *Lk = w.L + tri(kn);
                 iv_n = w.inv[kn];
 #pragma unroll
-                for (int t2 = 0; t2 < NT; ++t2) {
+                for (int t2 = 0; t2 <= tt; ++t2) {  // chunks > tt are final
                     const int c = gl + LPR * t2;
                     lk_n[t2] = Lk[c < kn ? c : 0];
                 }
             }
             const double gk = G.bcast(tb[tt] * iv, ln);
-            if (live && gl == ln) w.g[k] = gk;
+            if (live) {  // predicated: broadcast store and live-column folds
+                w.g[k] = gk;
 #pragma unroll
-            for (int t2 = 0; t2 <= tt; ++t2) {
-                const double nv = fma(-lk[t2], gk, tb[t2]);
-                tb[t2] = live ? nv : tb[t2];
+                for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
             }
         }
     }

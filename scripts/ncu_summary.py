@@ -1,0 +1,44 @@
+"""Compact text summary of one ncu --set full capture of a set-up kernel:
+speed-of-light / occupancy / scheduler metrics (details page), stall-reason
+shares (raw page) and, if the object file matching the capture is given, the
+top source lines by instructions (scripts/sass_lines.py).
+usage: ncu_summary.py details.csv raw.csv [sass.csv object.o mangled_kernel]"""
+import csv
+import subprocess
+import sys
+
+KEEP = {"Duration", "SM Frequency", "Elapsed Cycles", "Compute (SM) Throughput", "Memory Throughput",
+        "L1/TEX Hit Rate", "L2 Hit Rate", "DRAM Throughput", "Executed Ipc Active", "Issue Slots Busy",
+        "Registers Per Thread", "Block Size", "Grid Size", "Dynamic Shared Memory Per Block",
+        "Achieved Active Warps Per SM", "Theoretical Occupancy", "Active Warps Per Scheduler",
+        "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction", "Avg. Active Threads Per Warp",
+        "Avg. Not Predicated Off Threads Per Warp"}
+det = list(csv.reader(open(sys.argv[1])))
+hdr = det[0]
+ix = {h: i for i, h in enumerate(hdr)}
+kname = det[1][ix["Kernel Name"]] if "Kernel Name" in ix else "?"
+print(f"kernel: {kname}")
+seen = set()
+for r in det[1:]:
+    n = r[ix["Metric Name"]]
+    if n in KEEP and n not in seen:
+        seen.add(n)
+        print(f"  {n:45s} {r[ix['Metric Value']]:>16s} {r[ix['Metric Unit']]}")
+raw = list(csv.reader(open(sys.argv[2])))
+h, v = raw[0], raw[2]
+items = [(a, b) for a, b in zip(h, v) if "pcsamp_warps_issue_stalled" in a and not a.endswith("not_issued")]
+tot = sum(float(b.replace(",", "") or 0) for _, b in items)
+print("stall reasons (share of PC samples):")
+for a, b in sorted(items, key=lambda t: -float(t[1].replace(",", "") or 0))[:10]:
+    print(f"  {a.replace('smsp__pcsamp_warps_issue_stalled_', ''):30s} {100 * float(b.replace(',', '')) / tot:6.2f}%")
+for key in ("inst_executed", "sm__sass_thread_inst_executed_op_dfma_pred_on.sum",
+            "dram__bytes_read.sum", "dram__bytes_write.sum"):
+    for a, b in zip(h, v):
+        if a == key or a.startswith(key):
+            print(f"  {a:45s} {b}")
+            break
+if len(sys.argv) > 5:
+    print("top source lines:")
+    out = subprocess.run([sys.executable, __file__.replace("ncu_summary.py", "sass_lines.py"), sys.argv[3],
+                          sys.argv[4], sys.argv[5], "25"], capture_output=True, text=True).stdout
+    print(out)
