@@ -33,9 +33,11 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.M = M;
     w.CA = CA;
     double *d = reinterpret_cast<double *>(base);
+    // g first: the lockstep fast paths prefetch inv[-1] / y[-1] (unused values) and
+    // read up to 31 doubles past the end of L (into arow), all inside the row's region
+    w.g = d; d += M;
     w.inv = d; d += M;
     w.y = d; d += M;
-    w.g = d; d += M;
     w.L = d; d += (M * (M + 1)) / 2 + 1;
     w.arow = d; d += S * M;
     w.brow = d; d += S;

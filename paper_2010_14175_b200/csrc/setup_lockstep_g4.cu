@@ -1,0 +1,6 @@
+// setup_lockstep_g4.cu -- lockstep hit-list kernel instances with 4 new rows per bordering group.
+#include "setup_lockstep_impl.cuh"
+
+namespace afsai {
+template SetupKernFn ls_instance<4>(int lpr, int nt, int hc);
+}  // namespace afsai

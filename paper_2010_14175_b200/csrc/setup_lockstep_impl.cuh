@@ -1,4 +1,4 @@
-// setup_lockstep.cu -- hit-list set-up kernel, several rows per warp in LOCKSTEP.
+// setup_lockstep_impl.cuh -- hit-list set-up kernel, several rows per warp in LOCKSTEP.
 //
 // Same algorithm and arithmetic as setup_hits.cu (C1-C12), but the
 // 32/LPR rows of a warp advance together: every loop that contains a shuffle
@@ -11,6 +11,7 @@
 //    so the fixed per-stage cost (operand loads, the broadcast, the owner's
 //    store, the loop) is shared by four rows.
 // Used for short rows (<= LPR entries, stencils) and s <= 4.
+#pragma once
 #include "setup_hits.cuh"
 
 namespace afsai {
@@ -100,21 +101,43 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
     G.sync();
 }
 
-// border_group of setup_common.cuh in lockstep: the old-column stages run to the
-// warp maximum qf_max; a row's updates happen only while live (active && k < qf).
+// predicated fp64 fma: if (p) d = fma(a, b, d), as one predicated DFMA (no selects,
+// no temporaries; a plain `if` around fma() compiles to DFMA + two moves)
+__device__ __forceinline__ void fma_if(bool p, double a, double b, double &d) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
+        : "+d"(d)
+        : "d"(a), "d"(b), "r"((int)p));
+}
+
+// Bordered Cholesky of the new rows q = qf .. qf+gs-1 (arow slots ug..), forward
+// solve and psi update, in lockstep: the old-column stages run to the warp maximum
+// qf_max; a row's updates happen only while live (active && k < qf).
+//  - right-looking column sweep: at stage k the owner lane of column k turns its
+//    accumulator into L[q][k] = t * inv[k] and broadcasts it; every lane folds
+//    fma(-L[q][k], L[c][k], t_c) into its columns.  The owner multiplies by the
+//    inverse diagonal of its own column, held in a register (no per-stage load on
+//    the broadcast's critical path); the stage's shared-memory operands are
+//    loaded first and arrive during the DMUL -> SHFL.
+//  - finalized accumulators are dead: folded unpredicated (their loads read any
+//    in-bounds row of L).
+//  - the group's own columns (diagonal of each new row, couplings among the new
+//    rows) are kept redundantly in every lane.
+// Every accumulator folds in k-ascending order, exactly DESIGN.md C5.  One copy of
+// the stage per column chunk and no unrolling: the kernel is instruction-cache bound
+// when its code grows.  Returns false on a pivot !(> 1e-30).
 template <int LPR, int NT, int GS>
 __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool active, int qf, int gs, int ug,
                                 int qf_max, double &psi) {
     const int M = w.M, gl = G.gl;
-    double t[GS][NT];
-    double dg[GS], ty[GS];
-    double cp[GS][GS];
+    double t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
     double *Lnew[GS];
     const double *Lr[NT];
+    bool st[GS];
 #pragma unroll
     for (int u = 0; u < GS; ++u) {
         const double *ar = w.arow + (ug + u) * M;
         const bool ur = active && u < gs;
+        st[u] = ur;
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt) {
             const int c = gl + LPR * tt;
@@ -129,55 +152,39 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        Lr[tt] = (active && c < qf) ? w.L + tri(c) : w.inv;  // dead columns: any in-bounds row
+        const bool old = active && c < qf;
+        Lr[tt] = old ? w.L + tri(c) : w.L;  // dead columns: any in-bounds row
+        ivc[tt] = old ? w.inv[c] : 0.0;
     }
-    const int qlim = (active && qf > 0) ? qf - 1 : 0;  // clamp for the operand prefetch
-    double inv_n = w.inv[0], y_n = w.y[0], lsm_n[NT];
-#pragma unroll
-    for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][0];
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         int lnend = qf_max - LPR * tt;
         if (lnend > LPR) lnend = LPR;
-#pragma unroll 2
+#pragma unroll 1
         for (int ln = 0; ln < lnend; ++ln) {
             const int k = LPR * tt + ln;
             const bool live = active && k < qf;
-            const double inv_k = inv_n, y_k = y_n;
+            const double y_k = w.y[k];
             double lsm[NT];
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2) lsm[t2] = lsm_n[t2];
-            {
-                const int kn = (k + 1 < qlim) ? k + 1 : qlim;
-                inv_n = w.inv[kn];
-                y_n = w.y[kn];
-#pragma unroll
-                for (int t2 = tt; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];  // chunks < tt are dead
-            }
+            for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
             double l[GS];
 #pragma unroll
-            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
-            if (live) {  // broadcast value: every lane of the row stores the same bits
+            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
 #pragma unroll
-                for (int u = 0; u < GS; ++u)
-                    if (u < gs) Lnew[u][k] = l[u];
-            }
-            // t accumulators outside a row's live stages are dead (finalized old
-            // columns, or columns that are not old): updated unpredicated
+            for (int u = 0; u < GS; ++u)
+                if (live && st[u]) Lnew[u][k] = l[u];  // every lane of the row stores the same bits
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
                 for (int u = 0; u < GS; ++u) t[u][t2] = fma(-l[u], lsm[t2], t[u][t2]);
-            // live-stage updates as predicated fmas (no selects; signed zeros kept)
-            if (live) {
 #pragma unroll
-                for (int u = 0; u < GS; ++u) {
-                    dg[u] = fma(-l[u], l[u], dg[u]);
-                    ty[u] = fma(-l[u], y_k, ty[u]);
+            for (int u = 0; u < GS; ++u) {
+                fma_if(live, -l[u], l[u], dg[u]);
+                fma_if(live, -l[u], y_k, ty[u]);
 #pragma unroll
-                    for (int v = 0; v < GS; ++v)
-                        if (v < u) cp[u][v] = fma(-l[u], l[v], cp[u][v]);
-                }
+                for (int v = 0; v < GS; ++v)
+                    if (v < u) fma_if(live, -l[u], l[v], cp[u][v]);
             }
         }
     }
@@ -197,17 +204,15 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
             const double inv_k = 1.0 / dq;
             const double y_k = ty[uf] * inv_k;
             psi = fma(-y_k, y_k, psi);     // C6
-            if (gl == 0) {
-                w.inv[k] = inv_k;
-                w.y[k] = y_k;
-            }
+            w.inv[k] = inv_k;  // redundant values: every lane stores the same bits
+            w.y[k] = y_k;
             double lu[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) {
                 lu[u] = 0.0;
                 if (u > uf && u < gs) {
                     lu[u] = cp[u][uf] * inv_k;
-                    if (gl == 0) Lnew[u][k] = lu[u];
+                    Lnew[u][k] = lu[u];
                 }
             }
 #pragma unroll
@@ -226,62 +231,45 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
     return ok;
 }
 
-// back_substitute of setup_common.cuh in lockstep (stages to the warp maximum m_max)
+// Back-substitution g~ = L^-T y (C7) in lockstep (stages to the warp
+// maximum m_max): descending column sweep; lane c folds fma(-L[k][c], g[k], t_c) for
+// k = m-1 down to c+1.  Row k of L is read contiguously by the lanes (a running
+// pointer: tri(k-1) = tri(k) - k); reads past the row's live columns land inside the
+// row's shared-memory region (carve_hits: arow follows L) and feed dead
+// accumulators; a row's folds are predicated on its live stages (k < m).
 template <int LPR, int NT>
 __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool active, int m, int m_max) {
     const int gl = G.gl;
-    double tb[NT];
+    double tb[NT], ivc[NT];
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        tb[tt] = (active && c < m) ? w.y[c] : 0.0;
+        const bool in = active && c < m;
+        tb[tt] = in ? w.y[c] : 0.0;
+        ivc[tt] = in ? w.inv[c] : 0.0;
     }
-    const int mlim = (active && m > 0) ? m - 1 : 0;
-    double iv_n, lk_n[NT];
-    {
-        const int k0 = (m_max - 1 < mlim) ? m_max - 1 : mlim;
-        const int kk = k0 < 0 ? 0 : k0;
-        const double *Lk = w.L + tri(kk);
-        iv_n = w.inv[kk];
-#pragma unroll
-        for (int t2 = 0; t2 < NT; ++t2) {
-            const int c = gl + LPR * t2;
-            lk_n[t2] = Lk[c < kk ? c : 0];
-        }
-    }
+    const double *pk = w.L + tri(m_max > 0 ? m_max - 1 : 0) + gl;  // row k, this lane's first column
 #pragma unroll
     for (int tt = NT - 1; tt >= 0; --tt) {
         int ln0 = m_max - 1 - LPR * tt;
         if (ln0 > LPR - 1) ln0 = LPR - 1;
-#pragma unroll 2
+#pragma unroll 1
         for (int ln = ln0; ln >= 0; --ln) {
             const int k = LPR * tt + ln;
             const bool live = active && k < m;
-            const double iv = iv_n;
             double lk[NT];
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2) lk[t2] = lk_n[t2];
-            {
-                int kn = k - 1 < mlim ? k - 1 : mlim;
-                kn = kn < 0 ? 0 : kn;
-                const double *Lk = w.L + tri(kn);
-                iv_n = w.inv[kn];
+            for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];  // L[k][c]; c >= k: dead
+            pk -= k;
+            const double gk = G.bcast(tb[tt] * ivc[tt], ln);
+            if (live) w.g[k] = gk;  // broadcast value, stored by every lane of the row
 #pragma unroll
-                for (int t2 = 0; t2 <= tt; ++t2) {  // chunks > tt are final
-                    const int c = gl + LPR * t2;
-                    lk_n[t2] = Lk[c < kn ? c : 0];
-                }
-            }
-            const double gk = G.bcast(tb[tt] * iv, ln);
-            if (live) {  // predicated: broadcast store and live-column folds
-                w.g[k] = gk;
-#pragma unroll
-                for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
-            }
+            for (int t2 = 0; t2 <= tt; ++t2) fma_if(live, -lk[t2], gk, tb[t2]);
         }
     }
     G.sync();
 }
+
 
 template <int LPR, int NT, int GS, int HC>
 // 16 lanes per row: <= 170 registers (three warps per SMSP register file) and CTAs
@@ -563,37 +551,24 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
     }
 }
 
-// ---------------------------------------------------------------- host side
-template <int LPR, int NT, int HC>
-static SetupKernFn ls_gs(int gs) {
-    switch (gs) {
-        case 1: return afsai_setup_rows_lockstep_kernel<LPR, NT, 1, HC>;
-        case 2: return afsai_setup_rows_lockstep_kernel<LPR, NT, 2, HC>;
-        case 3: return afsai_setup_rows_lockstep_kernel<LPR, NT, 3, HC>;
-        default: return afsai_setup_rows_lockstep_kernel<LPR, NT, 4, HC>;
+// kernel instance with GS new rows per bordering group (one translation unit per
+// GS: setup_lockstep_g{1..4}.cu)
+template <int GS>
+SetupKernFn ls_instance(int lpr, int nt, int hc) {
+#define AFSAI_LS_NT(L, H)                                                 \
+    switch (nt) {                                                         \
+        case 1: return afsai_setup_rows_lockstep_kernel<L, 1, GS, H>;     \
+        case 2: return afsai_setup_rows_lockstep_kernel<L, 2, GS, H>;     \
+        case 3: return afsai_setup_rows_lockstep_kernel<L, 3, GS, H>;     \
+        case 4: return afsai_setup_rows_lockstep_kernel<L, 4, GS, H>;     \
+        case 5: return afsai_setup_rows_lockstep_kernel<L, 5, GS, H>;     \
+        default: return afsai_setup_rows_lockstep_kernel<L, 6, GS, H>;    \
     }
-}
-
-template <int LPR, int HC>
-static SetupKernFn ls_nt(int nt, int gs) {
-    switch (nt) {
-        case 1: return ls_gs<LPR, 1, HC>(gs);
-        case 2: return ls_gs<LPR, 2, HC>(gs);
-        case 3: return ls_gs<LPR, 3, HC>(gs);
-        case 4: return ls_gs<LPR, 4, HC>(gs);
-        case 5: return ls_gs<LPR, 5, HC>(gs);
-        default: return ls_gs<LPR, 6, HC>(gs);
+    if (lpr == 8) {
+        if (hc <= 6) { AFSAI_LS_NT(8, 6) } else { AFSAI_LS_NT(8, 8) }
     }
-}
-
-// lpr (8 or 16) lanes per row, 32/lpr rows per warp; rows <= lpr entries,
-// s <= 4, mmax <= 6 * lpr
-SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc) {
-    if (s > kMaxGroup || mmax > 6 * lpr) return nullptr;
-    const int m = mmax < 1 ? 1 : mmax;
-    const int nt = (m + lpr - 1) / lpr;
-    if (lpr == 8) return hc <= 6 ? ls_nt<8, 6>(nt, s) : ls_nt<8, 8>(nt, s);
-    return hc <= 6 ? ls_nt<16, 6>(nt, s) : ls_nt<16, 8>(nt, s);
+    if (hc <= 6) { AFSAI_LS_NT(16, 6) } else { AFSAI_LS_NT(16, 8) }
+#undef AFSAI_LS_NT
 }
 
 }  // namespace afsai
