@@ -46,12 +46,46 @@ struct LGroup {
 
 __device__ __forceinline__ int warp_max(int v) { return (int)__reduce_max_sync(kAll, (unsigned)(v < 0 ? 0 : v)); }
 
-// scan_row_hits of setup_hits.cu with the slot allocation made warp-uniform
+// Per-row bookkeeping of the hit-list tables, held in registers with identical
+// values in every lane of the row's group (updated from ballots; no shared-memory
+// round trips, atomics or barriers): keys in the table, active-slot high-water
+// mark, size of the free-slot stack; ovf = this lane saw a table overflow.
+struct RowBook {
+    int nkeys, hw, nf;
+    bool ovf;
+};
+
+// hit_insert of setup_hits.cuh; returns false when the list is full
+template <int HC>
+__device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, int32_t r, double v) {
+    const int CA = w.CA;
+    const int n = w.ahn[aa];
+    if (n >= HC) return false;
+    int pos = n;
+    while (pos > 0) {
+        const int qp = w.ahq[(pos - 1) * CA + aa];
+        const int32_t rp = qp < 0 ? 0x7fffffff : w.P[qp];
+        if (rp <= r) break;
+        w.ahq[pos * CA + aa] = (int8_t)qp;
+        w.hv[pos * CA + aa] = w.hv[(pos - 1) * CA + aa];
+        --pos;
+    }
+    w.ahq[pos * CA + aa] = (int8_t)q;
+    w.hv[pos * CA + aa] = v;
+    w.ahn[aa] = (int8_t)(n + 1);
+    return true;
+}
+
+// scan_row_hits of setup_hits.cu with the slot allocation made warp-uniform: the
+// entry (c, v) of row P_q (q = -1: row i itself) of every lane joins the row's
+// universe: a pattern column is gathered into the local system, an existing
+// candidate gets the hit (r = P_q, v), a new column becomes a candidate.  All
+// lanes of the warp call it (ballot); one barrier at the end publishes the
+// tables to the next call.
 template <int LPR, int HC>
 __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H, int log2H, int32_t i, bool valid,
-                                 int32_t c, double v, int q, double *arow_u, double *brow_u) {
+                                 int32_t c, double v, int q, double *arow_u, double *brow_u, RowBook &b) {
     const int CA = w.CA;
-    const int32_t r = q < 0 ? i : w.P[q < w.M ? q : 0];
     bool need = false;
     int sl = -1;
     if (valid) {
@@ -61,26 +95,25 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
         } else if (c < i) {
             bool ins;
             sl = hinsert(w.hkey, H, log2H, c, &ins);
-            if (sl < 0) w.misc[1] = 1;
+            if (sl < 0) b.ovf = true;
             else if (ins) need = true;
             else {
                 const int st = w.hval[sl];
                 if (st >= 0) {
                     if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
-                } else if (st <= -2) {
-                    hit_insert<HC>(w, -2 - st, q, r, v);     // existing candidate: new hit
+                } else if (st <= -2) {                      // existing candidate: new hit
+                    const int32_t r = q < 0 ? i : w.P[q < w.M ? q : 0];
+                    if (!hit_insert_ls<HC>(w, -2 - st, q, r, v)) b.ovf = true;
                 }                                            // st == -1: dropped (row overflowed)
             }
         }
     }
     const unsigned bal = G.ballot(need);
-    const int nf = w.misc[3], hw = w.misc[2];
-    G.sync();
     if (need) {
         const int rk = __popc(bal & ((1u << G.gl) - 1u));
-        const int aa = rk < nf ? w.afree[nf - 1 - rk] : hw + (rk - nf);
+        const int aa = rk < b.nf ? w.afree[b.nf - 1 - rk] : b.hw + (rk - b.nf);
         if (aa >= CA) {
-            w.misc[1] = 1;            // the row is retried with larger tables;
+            b.ovf = true;             // the row is retried with larger tables;
             w.hval[sl] = (int8_t)-1;  // the key must not decode as an active slot
         } else {
             w.hval[sl] = (int8_t)(-2 - aa);
@@ -90,14 +123,12 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
             w.ahq[aa] = (int8_t)q;
             w.hv[aa] = v;
         }
-        atomicAdd(&w.misc[0], 1);
     }
     const int k = __popc(bal);
-    if (G.gl == 0 && k) {
-        const int take = k < nf ? k : nf;
-        w.misc[3] = nf - take;
-        w.misc[2] = hw + (k - take);
-    }
+    const int take = k < b.nf ? k : b.nf;
+    b.nf -= take;
+    b.hw += k - take;
+    b.nkeys += k;
     G.sync();
 }
 
@@ -311,25 +342,21 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             w.hval[sl] = (int8_t)-1;  // no stale shared memory is ever decoded
         }
         for (int x = gl; x < CA; x += LPR) w.ahn[x] = 0;
-        if (gl == 0) {
-            w.misc[0] = 0;
-            w.misc[1] = 0;
-            w.misc[2] = 0;
-            w.misc[3] = 0;
-            w.dscr[0] = 0.0;
-        }
+        if (gl == 0) w.dscr[0] = 0.0;
+        RowBook bk{0, 0, 0, false};
         G.sync();
         {
             const bool vi = has && gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
             const double xi = vi ? __ldg(a.val + e0i + gl) : 0.0;
-            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr);
+            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr, bk);
         }
         const double a_ii = w.dscr[0];
         const double psi0 = a_ii;
         double psi = psi0;
         int m = 0, steps = 0, reason = AFSAI_STOP_KMAX, fail_step = 0;
-        bool fail = false, overflow = has && (w.misc[1] != 0);
+        const bool ovf0 = G.ballot(bk.ovf) != 0;  // full-warp ballot: every lane, before any && short-circuit
+        bool fail = false, overflow = has && ovf0;
         bool running = has && !overflow;
         PHASE(0)
         for (int k = 1; k <= a.nsteps; ++k) {
@@ -347,7 +374,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
 #pragma unroll
             for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = 0x7fffffff; bt[q] = -1; }
             if (running) {
-                const int hw = w.misc[2];
+                const int hw = bk.hw;
                 for (int aa = gl; aa < hw; aa += LPR) {
                     const int n = w.ahn[aa];
                     if (n == 0) continue;
@@ -417,12 +444,11 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                 w.gstart[rank] = g0;
                 w.glen[rank] = (int32_t)(g1 - g0);
                 w.ahn[aa] = 0;
-                w.afree[w.misc[3] + gl] = (int16_t)aa;
+                w.afree[bk.nf + gl] = (int16_t)aa;
             }
             for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = 0.0;
             if (gl < nsel) w.brow[gl] = 0.0;
-            G.sync();
-            if (gl == 0) w.misc[3] += nsel;
+            bk.nf += nsel;
             G.sync();
             PHASE(2)
             // ---- gather: new rows (one entry per lane), all loads in flight first
@@ -441,10 +467,11 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     if (ug + u < nsel_max)
                         scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + ug + u,
                                                   w.arow + ((ug + u) < a.s ? ug + u : 0) * w.M,
-                                                  w.brow + ((ug + u) < a.s ? ug + u : 0));
+                                                  w.brow + ((ug + u) < a.s ? ug + u : 0), bk);
             }
             PHASE(3)
-            if (running && (w.misc[1] != 0 || w.misc[0] * 4 > H * 3)) {
+            const bool ovf_any = G.ballot(bk.ovf) != 0;
+            if (running && (ovf_any || bk.nkeys * 4 > H * 3)) {
                 overflow = true;
                 running = false;
             }
@@ -527,7 +554,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     c_r1 += (reason == 1);
                     c_r2 += (reason == 2);
                     c_r3 += (reason == 3);
-                    c_univ = max(c_univ, (unsigned long long)w.misc[0]);
+                    c_univ = max(c_univ, (unsigned long long)bk.nkeys);
                 }
             }
         }
