@@ -14,6 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libafsai_b200.so")
 if os.environ.get("AFSAI_DEBUG_LIB") == "1":  # bounds-checked build (build.py --debug)
     LIB_PATH = os.path.join(HERE, "lib", "libafsai_b200_dbg.so")
+if os.environ.get("AFSAI_LIB"):  # A/B experiments against another build of the library
+    LIB_PATH = os.environ["AFSAI_LIB"]
 
 AFSAI_OK, AFSAI_EINVAL, AFSAI_ENOTSPD, AFSAI_ECUDA, AFSAI_ENCCL, AFSAI_ENOMEM, AFSAI_ENOTCONV, AFSAI_ELIMIT = range(8)
 STOP_NAMES = {0: "kmax", 1: "cap", 2: "no_candidates", 3: "tolerance"}

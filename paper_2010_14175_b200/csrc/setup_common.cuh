@@ -106,19 +106,20 @@ __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {
 // arow/brow slots ug .. ug+gs-1), forward solve and psi update.
 //  - old columns c < qf: right-looking column sweep.  At stage k the owner lane
 //    of column k turns its accumulator into L[q][k] = t * inv[k] and broadcasts
-//    it; every lane folds fma(-L[q][k], L[c][k], t_c) into its own columns.
-//    Accumulators of already finalized columns are dead, so the fold runs
-//    unpredicated (their loads read any in-bounds row: inv).
+//    it; every lane folds fma(-L[q][k], L[c][k], t_c) into its own columns.  The
+//    owner multiplies by its column's inverse diagonal, held in a register, and
+//    the stage's shared-memory operands are loaded first (they arrive during the
+//    DMUL -> SHFL), so no software pipelining is needed.  Accumulators of
+//    finalized columns are dead: folded unpredicated (loads of any in-bounds row).
 //  - new columns (the diagonal of each new row and the couplings between new
 //    rows) are few: every lane keeps them redundantly, no broadcast needed.
-// Every accumulator folds in k-ascending order, exactly DESIGN.md C5.
-// Returns false on a pivot !(> 1e-30).
+// One copy of the stage per column chunk, not unrolled (the set-up kernels are
+// instruction-cache sensitive).  Every accumulator folds in k-ascending order,
+// exactly DESIGN.md C5.  Returns false on a pivot !(> 1e-30).
 template <int LPR, int NT, int GS, class State>
 __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs, int ug, double &psi) {
     const int M = w.M, gl = G.gl;
-    double t[GS][NT];
-    double dg[GS], ty[GS];
-    double cp[GS][GS];  // cp[u][v], v < u: accumulator of L[q_u][q_v]
+    double t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
     double *Lnew[GS];
     const double *Lr[NT];
 #pragma unroll
@@ -133,46 +134,28 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 #pragma unroll
         for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && u < gs) ? ar[qf + v] : 0.0;
         ty[u] = (u < gs) ? -w.brow[ug + u] : 0.0;
-        Lnew[u] = w.L + tri(qf + u);
+        Lnew[u] = w.L + tri(qf + u < M ? qf + u : 0);
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        Lr[tt] = (c < qf) ? w.L + tri(c) : w.inv;  // dead columns: any in-bounds row
-    }
-    // ---- stages over the old columns k < qf.  The shared-memory operands of
-    //      stage k+1 are loaded during stage k (software pipelining), so a stage's
-    //      critical path is DMUL -> SHFL -> DFMA only.
-    double inv_n = 0.0, y_n = 0.0, lsm_n[NT];
-#pragma unroll
-    for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = 0.0;
-    if (qf > 0) {
-        inv_n = w.inv[0];
-        y_n = w.y[0];
-#pragma unroll
-        for (int t2 = 0; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][0];
+        Lr[tt] = (c < qf) ? w.L + tri(c) : w.L;  // dead columns: any in-bounds row
+        ivc[tt] = (c < qf) ? w.inv[c] : 0.0;
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         int lnend = qf - LPR * tt;
         if (lnend > LPR) lnend = LPR;
+#pragma unroll 1
         for (int ln = 0; ln < lnend; ++ln) {
             const int k = LPR * tt + ln;
-            const double inv_k = inv_n;
-            const double y_k = y_n;
+            const double y_k = w.y[k];
             double lsm[NT];
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2) lsm[t2] = lsm_n[t2];
-            {
-                const int kn = (k + 1 < qf) ? k + 1 : k;  // prefetch (clamped, in bounds)
-                inv_n = w.inv[kn];
-                y_n = w.y[kn];
-#pragma unroll
-                for (int t2 = tt; t2 < NT; ++t2) lsm_n[t2] = Lr[t2][kn];  // chunks < tt are dead
-            }
+            for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
             double l[GS];
 #pragma unroll
-            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * inv_k, ln);
+            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
             // broadcast values: every lane stores the same bits (no divergent branch
             // before the next stage's shuffles)
 #pragma unroll
@@ -231,52 +214,35 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 }
 
 // Back-substitution g~ = L^-T y (C7): descending column sweep; lane c
-// folds fma(-L[k][c], g[k], t_c) for k = m-1 down to c+1.  Accumulators with
-// c >= k are final (dead), so the fold is unpredicated; indices past the row are
-// clamped to stay inside L.
+// folds fma(-L[k][c], g[k], t_c) for k = m-1 down to c+1.  Row k of L is read
+// contiguously by the lanes through a running pointer (tri(k-1) = tri(k) - k);
+// reads past the row's live columns stay inside the row's shared-memory region
+// (every state layout puts arow and more after L) and feed dead accumulators
+// (c >= k: final), so the fold is unpredicated.  The owner multiplies by its
+// column's inverse diagonal, held in a register.
 template <int LPR, int NT, class State>
 __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
     const int gl = G.gl;
-    double tb[NT];
+    double tb[NT], ivc[NT];
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
         tb[tt] = (c < m) ? w.y[c] : 0.0;
+        ivc[tt] = (c < m) ? w.inv[c] : 0.0;
     }
-    // operands of stage k-1 are loaded during stage k (software pipelining)
-    double iv_n = 0.0, lk_n[NT];
-#pragma unroll
-    for (int t2 = 0; t2 < NT; ++t2) lk_n[t2] = 0.0;
-    if (m > 0) {
-        const double *Lk = w.L + tri(m - 1);
-        iv_n = w.inv[m - 1];
-#pragma unroll
-        for (int t2 = 0; t2 < NT; ++t2) {
-            const int c = gl + LPR * t2;
-            lk_n[t2] = Lk[c < m - 1 ? c : 0];
-        }
-    }
+    const double *pk = w.L + tri(m > 0 ? m - 1 : 0) + gl;
 #pragma unroll
     for (int tt = NT - 1; tt >= 0; --tt) {
         int ln0 = m - 1 - LPR * tt;
         if (ln0 > LPR - 1) ln0 = LPR - 1;
+#pragma unroll 1
         for (int ln = ln0; ln >= 0; --ln) {
             const int k = LPR * tt + ln;
-            const double iv = iv_n;
             double lk[NT];
 #pragma unroll
-            for (int t2 = 0; t2 < NT; ++t2) lk[t2] = lk_n[t2];
-            {
-                const int kn = k > 0 ? k - 1 : 0;
-                const double *Lk = w.L + tri(kn);
-                iv_n = w.inv[kn];
-#pragma unroll
-                for (int t2 = 0; t2 <= tt; ++t2) {  // chunks > tt are final
-                    const int c = gl + LPR * t2;
-                    lk_n[t2] = Lk[c < kn ? c : 0];
-                }
-            }
-            const double gk = G.bcast(tb[tt] * iv, ln);
+            for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];
+            pk -= k;
+            const double gk = G.bcast(tb[tt] * ivc[tt], ln);
             w.g[k] = gk;  // broadcast value, stored by every lane
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
