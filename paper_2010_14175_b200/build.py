@@ -46,10 +46,17 @@ def _flags_for(src: str):
     return flags
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
+    """variant + defines: an A/B build (extra -D flags) into build_obj_<variant>/ and
+    lib/libafsai_b200_<variant>.so, loaded with AFSAI_LIB=<path>."""
     objdir = OBJDIR_DBG if debug else OBJDIR
     lib_out = LIB_DBG if debug else LIB
     extra = ["-DAFSAI_BOUNDS_CHECK"] if debug else []
+    if variant:
+        objdir = os.path.join(HERE, "build_obj_" + variant)
+        lib_out = os.path.join(LIBDIR, f"libafsai_b200_{variant}.so")
+        extra = extra + ["-D" + d for d in defines]
     os.makedirs(LIBDIR, exist_ok=True)
     os.makedirs(objdir, exist_ok=True)
     inc, libdir = _nccl_dirs()
@@ -91,4 +98,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))
+    var = next((x.split("=", 1)[1] for x in sys.argv if x.startswith("--variant=")), "")
+    defs = tuple(x[2:] for x in sys.argv if x.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv,
+                variant=var, defines=defs))

@@ -8,7 +8,12 @@
 
 namespace afsai {
 
-constexpr int kProwDepth = 8;   // pattern rows prefetched ahead in the gradient
+#ifndef AFSAI_PROW_DEPTH
+#define AFSAI_PROW_DEPTH 6
+#endif
+// pattern rows prefetched ahead in the gradient: the value loads come from L2
+// (~600 cycles under load), a row's fold is one LDS -> DFMA -> STS chain
+constexpr int kProwDepth = AFSAI_PROW_DEPTH;
 constexpr int kProwGather = 8;  // entries per lane loaded per gather batch
 
 // Insert-if-absent of one key per lane (lanes with !valid idle).  The probe loop
@@ -49,7 +54,7 @@ __device__ __forceinline__ int hinsert_warp(int32_t *hkey, int H, int log2H, boo
 template <int NV>
 struct PRowFetch {
     double v[NV];
-    double *s[NV];  // &acc[slot]
+    int s[NV];  // acc slot (H: the spare slot); 32-bit to keep the prefetch depth in registers
     double gq;
 };
 
@@ -59,7 +64,7 @@ struct PRowFetch {
 // Branch-free: rows past m read row m's descriptor with no entries.  Lanes
 // without an entry fold 0 into the spare slot acc[H].
 template <int LPR, int NV>
-__device__ __forceinline__ void prow_fetch(const PRowState &w, const double *vrow, double *spare, int idx, int m,
+__device__ __forceinline__ void prow_fetch(const PRowState &w, const double *vrow, int spare, int idx, int m,
                                            int gl, PRowFetch<NV> &f) {
     const bool live = idx <= m;
     const int4 d = w.pd[live ? idx : m];
@@ -71,7 +76,7 @@ __device__ __forceinline__ void prow_fetch(const PRowState &w, const double *vro
     for (int v = 0; v < NV; ++v) {
         const int x = gl + LPR * v;
         const bool in = x < n;
-        f.s[v] = in ? w.acc + lb[x] : spare;
+        f.s[v] = in ? (int)lb[x] : spare;
         f.v[v] = in ? __ldg(vb + x) : 0.0;
     }
 }
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 PRowFetch<NV> pf[kProwDepth];
 #pragma unroll
                 const double *vrow = a.val + e0i;
-                double *const spare = w.acc + H;
+                const int spare = H;
 #pragma unroll
                 for (int d = 0; d < kProwDepth; ++d) prow_fetch<LPR, NV>(w, vrow, spare, d, m, gl, pf[d]);
                 for (int base = 0; base <= m; base += kProwDepth) {
@@ -180,11 +185,11 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                             // stores (one LDS -> DFMA -> STS chain per row).
                             double av[NV];
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) av[v] = *pf[d].s[v];
+                            for (int v = 0; v < NV; ++v) av[v] = w.acc[pf[d].s[v]];
 #pragma unroll
                             for (int v = 0; v < NV; ++v) av[v] = fma(pf[d].v[v], pf[d].gq, av[v]);
 #pragma unroll
-                            for (int v = 0; v < NV; ++v) *pf[d].s[v] = av[v];
+                            for (int v = 0; v < NV; ++v) w.acc[pf[d].s[v]] = av[v];
                             G.sync();
                             prow_fetch<LPR, NV>(w, vrow, spare, base + d + kProwDepth, m, gl, pf[d]);
                         }
