@@ -405,6 +405,16 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     }
                 }
             }
+            // row extents of the lane's local top-GS candidates, loaded now: they
+            // arrive during the group argmax, and the winners' are stored by their
+            // lanes (one L2 round trip per step less on the row's critical path)
+            int64_t rs[GS], re[GS];
+#pragma unroll
+            for (int q = 0; q < GS; ++q) {
+                const bool ok = bt[q] >= 0;
+                rs[q] = ok ? rp_of(a, bj[q]) : 0;
+                re[q] = ok ? rp_of(a, (int64_t)bj[q] + 1) : 0;
+            }
             nc = G.sum(nc);
             PHASE(1)
             if (running && nc == 0) {
@@ -414,40 +424,61 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             const int nsel = running ? (nc < room ? nc : room) : 0;
             const int nsel_max = warp_max(nsel);
             if (nsel_max == 0) continue;
-            // ---- selection: nsel_max rounds of group argmax over the list heads
-            for (int u = 0; u < nsel_max; ++u) {
-                double wa = ba[0];
-                int32_t wj = bj[0];
+            // ---- selection: nsel_max (<= GS) rounds of group argmax over the list
+            //      heads; every lane keeps the winners (selj) and their ranks in
+            //      registers, the winner's lane stores its slot and row extent
+            int32_t selj[GS];
 #pragma unroll
-                for (int o = LPR / 2; o > 0; o >>= 1) {
-                    const double oa = G.xorv(wa, o);
-                    const int32_t oj = G.xorv(wj, o);
-                    if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
-                }
-                if (u < nsel && bj[0] == wj) {
-                    w.sel[u] = wj;
-                    w.sela[u] = bt[0];
+            for (int u = 0; u < GS; ++u) {
+                selj[u] = 0x7fffffff;
+                if (u < nsel_max) {
+                    double wa = ba[0];
+                    int32_t wj = bj[0];
 #pragma unroll
-                    for (int q = 0; q + 1 < GS; ++q) { ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1]; }
-                    ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                    for (int o = LPR / 2; o > 0; o >>= 1) {
+                        const double oa = G.xorv(wa, o);
+                        const int32_t oj = G.xorv(wj, o);
+                        if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
+                    }
+                    if (u < nsel) selj[u] = wj;
+                    if (u < nsel && bj[0] == wj) {
+                        w.sela[u] = bt[0];
+                        w.gstart[u] = rs[0];
+                        w.glen[u] = (int32_t)(re[0] - rs[0]);
+#pragma unroll
+                        for (int q = 0; q + 1 < GS; ++q) {
+                            ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1];
+                            rs[q] = rs[q + 1]; re[q] = re[q + 1];
+                        }
+                        ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                    }
                 }
             }
+            // new columns join P in ascending order: winner u goes to position m + rk[u]
+            int rk[GS];
+#pragma unroll
+            for (int u = 0; u < GS; ++u) {
+                rk[u] = 0;
+#pragma unroll
+                for (int v = 0; v < GS; ++v) rk[u] += (selj[v] < selj[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < GS; ++u)
+                for (int c = gl; c < m + nsel; c += LPR) w.arow[u * w.M + c] = 0.0;  // what border reads
+            if (gl < nsel) w.brow[gl] = 0.0;
             G.sync();
             if (gl < nsel) {
-                const int32_t j = w.sel[gl];
-                int rank = 0;
-                for (int u = 0; u < nsel; ++u) rank += (w.sel[u] < j);
+                int32_t j = selj[0];
+                int r = rk[0];
+#pragma unroll
+                for (int u = 1; u < GS; ++u)
+                    if (gl == u) { j = selj[u]; r = rk[u]; }
                 const int aa = w.sela[gl];
-                w.P[m + rank] = j;
-                w.hval[w.ahs[aa]] = (int8_t)(m + rank);
-                const int64_t g0 = rp_of(a, j), g1 = rp_of(a, (int64_t)j + 1);
-                w.gstart[rank] = g0;
-                w.glen[rank] = (int32_t)(g1 - g0);
+                w.P[m + r] = j;
+                w.hval[w.ahs[aa]] = (int8_t)(m + r);
                 w.ahn[aa] = 0;
                 w.afree[bk.nf + gl] = (int16_t)aa;
             }
-            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = 0.0;
-            if (gl < nsel) w.brow[gl] = 0.0;
             bk.nf += nsel;
             G.sync();
             PHASE(2)
@@ -464,10 +495,11 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                 }
 #pragma unroll
                 for (int u = 0; u < GS; ++u)
-                    if (ug + u < nsel_max)
-                        scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + ug + u,
-                                                  w.arow + ((ug + u) < a.s ? ug + u : 0) * w.M,
-                                                  w.brow + ((ug + u) < a.s ? ug + u : 0), bk);
+                    if (ug + u < nsel_max) {  // winner u (selection order) is pattern position m + rk[u]
+                        const int r = rk[u] < GS ? rk[u] : 0;
+                        scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + r,
+                                                  w.arow + r * w.M, w.brow + r, bk);
+                    }
             }
             PHASE(3)
             const bool ovf_any = G.ballot(bk.ovf) != 0;
