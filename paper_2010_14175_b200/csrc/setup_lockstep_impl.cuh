@@ -428,9 +428,15 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             //      heads; every lane keeps the winners (selj) and their ranks in
             //      registers, the winner's lane stores its slot and row extent
             int32_t selj[GS];
+            int32_t pc[GS];
+            double pv[GS];
+            bool pvld[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) {
                 selj[u] = 0x7fffffff;
+                pvld[u] = false;
+                pc[u] = 0;
+                pv[u] = 0.0;
                 if (u < nsel_max) {
                     double wa = ba[0];
                     int32_t wj = bj[0];
@@ -441,10 +447,18 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                         if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
                     }
                     if (u < nsel) selj[u] = wj;
-                    if (u < nsel && bj[0] == wj) {
+                    // the winner's row entries are loaded right away (one per lane):
+                    // they arrive during the next round and the bookkeeping below
+                    const bool won = u < nsel && bj[0] == wj;
+                    const unsigned wb = G.ballot(won);
+                    const int wl = wb ? __ffs(wb) - 1 : 0;
+                    const int64_t g0 = G.bcast(rs[0], wl);
+                    const int gn = G.bcast((int)(re[0] - rs[0]), wl);
+                    pvld[u] = (u < nsel) && gl < gn;
+                    pc[u] = pvld[u] ? __ldg(a.col + g0 + gl) : 0;
+                    pv[u] = pvld[u] ? __ldg(a.val + g0 + gl) : 0.0;
+                    if (won) {
                         w.sela[u] = bt[0];
-                        w.gstart[u] = rs[0];
-                        w.glen[u] = (int32_t)(re[0] - rs[0]);
 #pragma unroll
                         for (int q = 0; q + 1 < GS; ++q) {
                             ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1];
@@ -482,17 +496,8 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             bk.nf += nsel;
             G.sync();
             PHASE(2)
-            // ---- gather: new rows (one entry per lane), all loads in flight first
-            for (int ug = 0; ug < nsel_max; ug += GS) {
-                int32_t pc[GS];
-                double pv[GS];
-                bool pvld[GS];
-#pragma unroll
-                for (int u = 0; u < GS; ++u) {
-                    pvld[u] = (ug + u < nsel) && gl < w.glen[ug + u];
-                    pc[u] = pvld[u] ? __ldg(a.col + w.gstart[ug + u] + gl) : 0;
-                    pv[u] = pvld[u] ? __ldg(a.val + w.gstart[ug + u] + gl) : 0.0;
-                }
+            // ---- gather: new rows (one entry per lane, loaded during the selection)
+            for (int ug = 0; ug < nsel_max; ug += GS) {  // nsel_max <= GS: one pass
 #pragma unroll
                 for (int u = 0; u < GS; ++u)
                     if (ug + u < nsel_max) {  // winner u (selection order) is pattern position m + rk[u]
