@@ -376,8 +376,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             if (running) {
                 const int hw = bk.hw;
                 for (int aa = gl; aa < hw; aa += LPR) {
-                    const int n = w.ahn[aa];
-                    if (n == 0) continue;
+                    const int n = w.ahn[aa];  // 0: a freed slot (acc stays +0.0)
                     double acc = 0.0;
 #pragma unroll
                     for (int h = 0; h < HC; ++h) {
@@ -388,20 +387,22 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                         }
                     }
                     c_gfma += n;
-                    if (acc != 0.0) {
-                        ++nc;
-                        double ca = fabs(acc);
-                        int32_t cj = w.akey[aa];
-                        int32_t ct = aa;
+                    // branch-free insertion into the sorted top-GS list (selects)
+                    const bool cand = acc != 0.0;
+                    nc += cand;
+                    double ca = cand ? fabs(acc) : -1.0;
+                    int32_t cj = cand ? w.akey[aa] : 0x7fffffff, ct = aa;
 #pragma unroll
-                        for (int q = 0; q < GS; ++q) {
-                            if (better(ca, cj, ba[q], bj[q])) {
-                                const double ta = ba[q];
-                                const int32_t tj = bj[q], t2 = bt[q];
-                                ba[q] = ca; bj[q] = cj; bt[q] = ct;
-                                ca = ta; cj = tj; ct = t2;
-                            }
-                        }
+                    for (int q = 0; q < GS; ++q) {
+                        const bool b = better(ca, cj, ba[q], bj[q]);
+                        const double ta = ba[q];
+                        const int32_t tj = bj[q], t2 = bt[q];
+                        ba[q] = b ? ca : ba[q];
+                        bj[q] = b ? cj : bj[q];
+                        bt[q] = b ? ct : bt[q];
+                        ca = b ? ta : ca;
+                        cj = b ? tj : cj;
+                        ct = b ? t2 : ct;
                     }
                 }
             }
