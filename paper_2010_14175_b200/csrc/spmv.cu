@@ -78,8 +78,23 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
         double acc = 0.0;
         if (row < a.n) {
             const int64_t e1 = a.rowptr[row + 1];
-            for (int64_t e = a.rowptr[row] + sub; e < e1; e += W)
-                acc = fma(__ldg(a.val + e), __ldg(a.x + (__ldg(a.col + e) - a.x_off)), acc);
+            int64_t e = a.rowptr[row] + sub;
+            // four entries per lane in flight (column loads, then the x gathers),
+            // folded in the same ascending order as the plain loop
+            for (; e + 3 * W < e1; e += 4 * W) {
+                int32_t c[4];
+                double v[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    c[u] = __ldg(a.col + e + u * W);
+                    v[u] = __ldg(a.val + e + u * W);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = __ldg(a.x + (c[u] - a.x_off));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fma(v[u], xv[u], acc);
+            }
+            for (; e < e1; e += W) acc = fma(__ldg(a.val + e), __ldg(a.x + (__ldg(a.col + e) - a.x_off)), acc);
         }
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFullS, acc, o);
