@@ -217,6 +217,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     bool first = true;
     // One pass of the current plan over rows (device list) or [row_lo, row_lo+n);
     // returns the number of rows that overflowed an on-chip table in *rc.
+    unsigned long long why = 0;  // overflow reasons of the last pass (lockstep kernel): 1 table, 2 slots, 4 hits
     auto pass = [&](const int64_t *rows, int64_t n, int32_t *rc) -> int {
         if (H > (1 << 15)) return set_status(status, AFSAI_ELIMIT, "candidate table would exceed 32768 slots");
         a.H = H;
@@ -273,6 +274,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemsetAsync(W.counters.as<unsigned long long>() + 20, 0, sizeof(unsigned long long),
+                                       ctx->stream));
         if (std::getenv("AFSAI_DEBUG_PLAN"))
             std::fprintf(stderr,
                          "[afsai rank %d] pass: kernel=%s rows=%lld list=%d H=%d cact=%d lpr=%d rb=%lld "
@@ -287,6 +290,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         }
         ctx->launches += 1;
         AFSAI_CUDA_TRY(cudaMemcpyAsync(rc, W.retry_count.p, sizeof *rc, cudaMemcpyDeviceToHost, ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(&why, W.counters.as<unsigned long long>() + 20, sizeof why,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
         AFSAI_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         return AFSAI_OK;
     };
@@ -308,9 +313,15 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             if (r != AFSAI_OK) return r;
             first = false;
             if (rc * 100 <= ns) break;
-            if (2 * cact > kMaxCact || hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 > 200 * 1024) break;
-            H *= 2;
-            cact *= 2;
+            // grow what overflowed (the lockstep kernel reports why; others: both)
+            int nH = H, nC = cact;
+            if (!(hits && lockstep) || why == 0) why = 3;
+            if (why & 1) nH = 2 * H;
+            if (why & 2) nC = std::min(kMaxCact, cact + std::max(8, cact / 2));
+            if (nH == H && nC == cact) break;  // hit lists full: the retries take those rows
+            if (hits_row_bytes(nH, mmax, p.s, nC, hc) * 2 > 200 * 1024) break;
+            H = nH;
+            cact = nC;
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.counters.p, 0, 32 * sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.err.p, 0xff, sizeof(unsigned long long), ctx->stream));

@@ -53,6 +53,7 @@ __device__ __forceinline__ int warp_max(int v) { return (int)__reduce_max_sync(k
 struct RowBook {
     int nkeys, hw, nf;
     bool ovf;
+    unsigned why;  // overflow reasons: 1 hash table, 2 active candidate slots, 4 hit list
 };
 
 // hit_insert of setup_hits.cuh; returns false when the list is full
@@ -95,7 +96,7 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
         } else if (c < i) {
             bool ins;
             sl = hinsert(w.hkey, H, log2H, c, &ins);
-            if (sl < 0) b.ovf = true;
+            if (sl < 0) { b.ovf = true; b.why |= 1u; }
             else if (ins) need = true;
             else {
                 const int st = w.hval[sl];
@@ -103,7 +104,7 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
                     if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
                 } else if (st <= -2) {                      // existing candidate: new hit
                     const int32_t r = q < 0 ? i : w.P[q < w.M ? q : 0];
-                    if (!hit_insert_ls<HC>(w, -2 - st, q, r, v)) b.ovf = true;
+                    if (!hit_insert_ls<HC>(w, -2 - st, q, r, v)) { b.ovf = true; b.why |= 4u; }
                 }                                            // st == -1: dropped (row overflowed)
             }
         }
@@ -114,6 +115,7 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
         const int aa = rk < b.nf ? w.afree[b.nf - 1 - rk] : b.hw + (rk - b.nf);
         if (aa >= CA) {
             b.ovf = true;             // the row is retried with larger tables;
+            b.why |= 2u;
             w.hval[sl] = (int8_t)-1;  // the key must not decode as an active slot
         } else {
             w.hval[sl] = (int8_t)(-2 - aa);
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
         }
         for (int x = gl; x < CA; x += LPR) w.ahn[x] = 0;
         if (gl == 0) w.dscr[0] = 0.0;
-        RowBook bk{0, 0, 0, false};
+        RowBook bk{0, 0, 0, false, 0u};
         G.sync();
         {
             const bool vi = has && gl < (int)(e1i - e0i);
@@ -510,6 +512,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             PHASE(3)
             const bool ovf_any = G.ballot(bk.ovf) != 0;
             if (running && (ovf_any || bk.nkeys * 4 > H * 3)) {
+                if (bk.nkeys * 4 > H * 3) bk.why |= 1u;
                 overflow = true;
                 running = false;
             }
@@ -552,9 +555,11 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             PHASE(5)
         }
         // ---- per-row outcome (no shuffles below until the final sync)
+        const unsigned whyw = __reduce_or_sync(kAll, overflow ? bk.why : 0u);  // both rows' reasons
         if (has) {
             if (overflow) {
                 if (gl == 0) {
+                    atomicOr(&a.counters[20], (unsigned long long)whyw);  // the host's table sizing
                     const int p = atomicAdd(a.retry_count, 1);
                     a.retry_rows[p] = i64;
                 }
