@@ -613,7 +613,8 @@ int dist_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z, af
 }
 
 // PCG on N GPUs (R12, §6): same recurrence as local_pcg; dot products
-// are reduced locally by the producing kernel and all-reduced (one double each).
+// are reduced locally by the producing kernel and all-reduced: p.q, then r.r and
+// r.z together (two all-reduces per iteration).
 int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const double *b_in, double *x, double tol,
              int32_t max_iters, afsai_pcg_report_t *rep, afsai_status_t *status) {
     if (!F->dist) return set_status(status, AFSAI_EINVAL, "factor was not built on this communicator");
@@ -661,6 +662,11 @@ int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const do
         AFSAI_NCCL_TRY(ncclAllReduce(&S->sum[k], &S->sum[k], 1, ncclDouble, ncclSum, ctx->comm, st));
         return AFSAI_OK;
     };
+    auto allreduce2 = [&](int k) -> int {  // sum[k], sum[k+1]
+        KTimer kt(ctx, AFSAI_K_COMM);
+        AFSAI_NCCL_TRY(ncclAllReduce(&S->sum[k], &S->sum[k], 2, ncclDouble, ncclSum, ctx->comm, st));
+        return AFSAI_OK;
+    };
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
     {
         KTimer kt(ctx, AFSAI_K_VECTOR);
@@ -700,11 +706,12 @@ int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const do
                 KTimer kt(ctx, AFSAI_K_VECTOR);
                 launch_pcg_axpy_dist(n, xd, r, p, q, parts, cnt, S, grid, st);  // sum[1] = r.r
             }
-            if ((rc = allreduce(1))) return rc;
-            launch_pcg_check_dist(S, tol, max_iters, st);
             rc = dist_apply_ext(ctx, F, re, te, z, r, &W, status);  // sum[2] = r.z
             if (rc) return rc;
-            if ((rc = allreduce(2))) return rc;
+            // r.r and r.z in one all-reduce; the convergence test on r.r follows it
+            // (same value, same iteration count; the converged iteration's apply runs)
+            if ((rc = allreduce2(1))) return rc;
+            launch_pcg_check_dist(S, tol, max_iters, st);
             {
                 KTimer kt(ctx, AFSAI_K_VECTOR);
                 launch_pcg_update_p_dist(n, p, z, S, 0, grid, st);
