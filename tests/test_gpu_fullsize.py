@@ -58,3 +58,14 @@ def test_M4_full_size_sampled(ctx):
     A = cfg["make"]()
     F, dA = sampled_parity(ctx, A, cfg["nsteps"], cfg["s"], cfg["max_row_nnz"], 150, 2)
     F.close()
+
+
+def test_M3_full_size_sampled(ctx):
+    """M3 (8M rows, anisotropic coefficients): exercises the overflow-reason table
+    sizing (256 table slots, 84 active slots) and its retries at full size."""
+    cfg = ai.CONFIGS["M3"]
+    A = cfg["make"]()
+    F, dA = sampled_parity(ctx, A, cfg["nsteps"], cfg["s"], cfg["max_row_nnz"], 400, 3)
+    st = F.stats()
+    assert st["table_size"] >= 256
+    F.close()
