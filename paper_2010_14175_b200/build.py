@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import glob
 import os
+import re
 import subprocess
 import sys
 
@@ -38,11 +39,19 @@ def _nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
+_CONTRACT_HDR = re.compile(r'#include\s+"setup_\w*\.cuh"')
+
+
 def _flags_for(src: str):
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
              "-Xptxas", "-v"] + ARCH
-    if os.path.basename(src).startswith("setup_"):
-        flags += ["-fmad=false"]
+    # Every unit that includes set-up device code (setup_*.cuh) compiles with
+    # -fmad=false, so the only fused multiply-adds are the explicit fma() of the
+    # arithmetic contract.  The decision is made from the file's
+    # includes, not its name; setup_common.cuh #errors without AFSAI_FMAD_OFF.
+    with open(src) as f:
+        if _CONTRACT_HDR.search(f.read()):
+            flags += ["-fmad=false", "-DAFSAI_FMAD_OFF"]
     return flags
 
 

@@ -46,7 +46,11 @@ int set_status(afsai_status_t *st, int code, const std::string &msg, int64_t row
                                        std::string(#expr " failed: ") + ncclGetErrorString(_r));    \
     } while (0)
 
-// Stream-ordered device buffer (cudaMallocAsync on the context stream).
+// The library's own stream-ordered memory pool on the current device (created by
+// the first context on the device; the device's default pool is never touched).
+cudaMemPool_t library_pool();
+
+// Stream-ordered device buffer (allocated from library_pool() on the context stream).
 struct DevBuf {
     void *p = nullptr;
     size_t bytes = 0;
@@ -69,7 +73,8 @@ struct DevBuf {
         stream = s;
         bytes = nbytes;
         if (nbytes == 0) return cudaSuccess;
-        return cudaMallocAsync(&p, nbytes, s);
+        cudaMemPool_t pool = library_pool();
+        return pool ? cudaMallocFromPoolAsync(&p, nbytes, pool, s) : cudaMallocAsync(&p, nbytes, s);
     }
     void release() {
         if (p) cudaFreeAsync(p, stream);
@@ -117,6 +122,7 @@ struct afsai_ctx_s {
     ncclComm_t comm = nullptr;  // null on one GPU
     int32_t rank = 0, nranks = 1;
     int64_t launches = 0;       // kernels launched by this library on this context
+    bool pool_held = false;     // holds a reference on the device's library pool
     cudaEvent_t ev[8] = {};
     // optional per-class kernel timing (afsai_ctx_set_timing)
     bool timing = false;
@@ -186,6 +192,7 @@ struct afsai_factor_s {
     int64_t gt_hi = 0;  // max column + 1 of G^T over local rows
     afsai::PcgWork pcg;
     void *dist = nullptr;  // multi-GPU halo plans (dist.cu)
+    bool block = false;    // made by afsai_setup_block: G rows only (no G^T), not appliable
     // device copy of a HOST A staged by afsai_setup, reused by afsai_pcg when
     // it is called with the same host arrays (one H2D of A per solve cycle)
     afsai::DeviceCsr staged_A;

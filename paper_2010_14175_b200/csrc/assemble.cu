@@ -228,7 +228,13 @@ __global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const in
     }
 }
 
-// warp per row of G^T: rank sort by column (row index of G), ascending (C10)
+// Rows of G^T are sorted by source row (C10): the scatter above places entries
+// in atomic (arbitrary) order.  Short rows (<= kLongRow entries, every stencil and
+// FE row) are rank-sorted by one warp; a hub column can make a G^T row as long
+// as n, so longer rows take an O(k log^2 k) CTA sort (sort_long_rows_kernel).
+constexpr int kLongRow = 256;
+
+// warp per short row of G^T: rank sort by column (row index of G), ascending
 __global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *in_col, const double *in_val,
                                  int32_t *out_col, double *out_val) {
     const int lane = threadIdx.x & 31;
@@ -237,6 +243,7 @@ __global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const in
     for (int64_t r = warp; r < n_rows; r += nw) {
         const int64_t o = rowptr[r];
         const int k = (int)(rowptr[r + 1] - o);
+        if (k > kLongRow) continue;  // sort_long_rows_kernel
         for (int t = lane; t < k; t += 32) {
             const int32_t c = in_col[o + t];
             int rank = 0;
@@ -245,6 +252,90 @@ __global__ void sort_rows_kernel(int64_t n_rows, const int64_t *rowptr, const in
             out_val[o + rank] = in_val[o + t];
         }
     }
+}
+
+// first index in the sorted run key[0, len) with key >= x
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *key, int64_t len, int32_t x) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (key[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// One CTA per long row (> kLongRow entries).  Keys (source rows) are unique in a
+// row, so the sorted order is unique.  Tiles of kSortTile keys are rank-sorted in
+// shared memory into out_*, then runs are merged pairwise (each element's place
+// = its index in its run + its rank in the partner run, a binary search), ping-
+// ponging between out_* and in_* (in_* is scratch); the result ends in out_*.
+constexpr int kSortTile = 1024;
+__global__ void __launch_bounds__(256) sort_long_rows_kernel(int64_t n_rows, const int64_t *rowptr, int32_t *in_col,
+                                                             double *in_val, int32_t *out_col, double *out_val) {
+    __shared__ int32_t skey[kSortTile];
+    __shared__ int64_t slist[256];
+    __shared__ int nlist;
+    for (int64_t r0 = (int64_t)blockIdx.x * 256; r0 < n_rows; r0 += (int64_t)gridDim.x * 256) {
+        if (threadIdx.x == 0) nlist = 0;
+        __syncthreads();
+        const int64_t r = r0 + threadIdx.x;
+        if (r < n_rows && rowptr[r + 1] - rowptr[r] > kLongRow) slist[atomicAdd(&nlist, 1)] = r;
+        __syncthreads();
+        const int nl = nlist;
+        for (int li = 0; li < nl; ++li) {
+            const int64_t row = slist[li];
+            const int64_t o = rowptr[row], k = rowptr[row + 1] - o;
+            // tiles: rank sort in shared memory, in_* -> out_*
+            for (int64_t t0 = 0; t0 < k; t0 += kSortTile) {
+                const int tl = (int)(k - t0 < kSortTile ? k - t0 : kSortTile);
+                for (int t = threadIdx.x; t < tl; t += blockDim.x) skey[t] = in_col[o + t0 + t];
+                __syncthreads();
+                for (int t = threadIdx.x; t < tl; t += blockDim.x) {
+                    const int32_t c = skey[t];
+                    int rank = 0;
+                    for (int u = 0; u < tl; ++u) rank += (skey[u] < c);
+                    out_col[o + t0 + rank] = c;
+                    out_val[o + t0 + rank] = in_val[o + t0 + t];
+                }
+                __syncthreads();
+            }
+            // merge passes
+            int32_t *sc = out_col + o, *dc = in_col + o;
+            double *sv = out_val + o, *dv = in_val + o;
+            for (int64_t w = kSortTile; w < k; w *= 2) {
+                for (int64_t p = threadIdx.x; p < k; p += blockDim.x) {
+                    const int64_t s0 = (p / (2 * w)) * (2 * w);
+                    const int64_t aend = s0 + w < k ? s0 + w : k, bend = s0 + 2 * w < k ? s0 + 2 * w : k;
+                    const int32_t x = sc[p];
+                    int64_t pos;
+                    if (p < aend) pos = (p - s0) + lower_bound_i32(sc + aend, bend - aend, x);
+                    else pos = (p - aend) + lower_bound_i32(sc + s0, aend - s0, x);
+                    dc[s0 + pos] = x;
+                    dv[s0 + pos] = sv[p];
+                }
+                __syncthreads();
+                int32_t *tc = sc; sc = dc; dc = tc;
+                double *tv = sv; sv = dv; dv = tv;
+            }
+            if (sc != out_col + o) {
+                for (int64_t p = threadIdx.x; p < k; p += blockDim.x) {
+                    out_col[o + p] = sc[p];
+                    out_val[o + p] = sv[p];
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+void sort_gt_rows(int64_t n_rows, const int64_t *rowptr, int32_t *in_col, double *in_val, int32_t *out_col,
+                  double *out_val, int grid, cudaStream_t st, int64_t *launches) {
+    sort_rows_kernel<<<grid, 256, 0, st>>>(n_rows, rowptr, in_col, in_val, out_col, out_val);
+    const int64_t g2 = (n_rows + 255) / 256;
+    sort_long_rows_kernel<<<(unsigned)(g2 < grid ? (g2 > 0 ? g2 : 1) : grid), 256, 0, st>>>(n_rows, rowptr, in_col,
+                                                                                              in_val, out_col, out_val);
+    *launches += 2;
 }
 
 // ---------------------------------------------------------------- multi-GPU helpers

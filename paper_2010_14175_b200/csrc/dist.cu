@@ -13,8 +13,8 @@
 //    send/recv of (col, row, val) triples); each rank builds its G^T rows sorted
 //    by source row.
 //  - PCG: per iteration three range halos (p for A p: [b - beta_A, e + beta_A);
-//    r for G r: [b - beta_G, b); t for G^T t: [e, e + beta_G)) and three
-//    one-double all-reduces (p.q, r.r, r.z).  Contiguous ranges need no packing:
+//    r for G r: [b - beta_G, b); t for G^T t: [e, e + beta_G)) and two
+//    all-reduces (p.q; then r.r and r.z packed in one).  Contiguous ranges need no packing:
 //    NCCL sends and receives straight from/into the extended vectors.
 #include <cuda_runtime.h>
 #include <nccl.h>
@@ -71,12 +71,32 @@ static ncclResult_t range_exchange(const RangePlan &P, void *ext, size_t elem, n
     if (r != ncclSuccess) return r;
     for (const Seg &s : P.recvs)
         if ((r = ncclRecv(base + (s.begin - P.lo) * elem, s.count * elem, ncclChar, s.peer, comm, st)) != ncclSuccess)
-            return r;
-    for (const Seg &s : P.sends)
-        if ((r = ncclSend(base + (s.begin - P.lo) * elem, s.count * elem, ncclChar, s.peer, comm, st)) != ncclSuccess)
-            return r;
-    return ncclGroupEnd();
+            break;
+    if (r == ncclSuccess)
+        for (const Seg &s : P.sends)
+            if ((r = ncclSend(base + (s.begin - P.lo) * elem, s.count * elem, ncclChar, s.peer, comm, st)) !=
+                ncclSuccess)
+                break;
+    const ncclResult_t r2 = ncclGroupEnd();  // always close the group
+    return r != ncclSuccess ? r : r2;
 }
+
+// an NCCL group that is always closed, also when a call inside it fails
+struct NcclGroup {
+    bool open = false;
+    ncclResult_t start() {
+        const ncclResult_t r = ncclGroupStart();
+        open = r == ncclSuccess;
+        return r;
+    }
+    ncclResult_t end() {
+        open = false;
+        return ncclGroupEnd();
+    }
+    ~NcclGroup() {
+        if (open) ncclGroupEnd();
+    }
+};
 
 struct DistState {
     std::vector<int64_t> bounds;  // nranks + 1
@@ -127,6 +147,23 @@ static int allreduce_max(afsai_ctx_t ctx, int64_t v, int64_t *out, afsai_status_
     int rc = allgather_i64(ctx, v, all, status);
     if (rc) return rc;
     *out = *std::max_element(all.begin(), all.end());
+    return AFSAI_OK;
+}
+
+// Error agreement: after a step that can fail on one rank only (staging,
+// validation, an allocation, a non-SPD row), every rank learns whether any rank
+// failed, so no rank walks into a collective a failed rank will never join.
+// Returns rc if this rank failed, else the lowest failing rank's code (AFSAI_OK if none).
+static int agree(afsai_ctx_t ctx, int rc, afsai_status_t *status) {
+    std::vector<int64_t> all;
+    afsai_status_t tmp{};
+    const int r2 = allgather_i64(ctx, rc, all, &tmp);
+    if (r2) return rc ? rc : set_status(status, r2, tmp.msg);
+    if (rc) return rc;
+    for (int q = 0; q < ctx->nranks; ++q)
+        if (all[q])
+            return set_status(status, (int)all[q],
+                              "rank " + std::to_string(q) + " failed (" + afsai_strerror((int)all[q]) + ")");
     return AFSAI_OK;
 }
 
@@ -222,7 +259,8 @@ static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<in
                                    cudaMemcpyDeviceToDevice, st));
     {
         KTimer kt(ctx, AFSAI_K_COMM);
-        AFSAI_NCCL_TRY(ncclGroupStart());
+        NcclGroup grp;
+        AFSAI_NCCL_TRY(grp.start());
         for (const Seg &s : P.recvs) {
             const int64_t e0 = hrp[s.begin - lo], e1 = hrp[s.begin + s.count - lo];
             AFSAI_NCCL_TRY(ncclRecv(X->b_col.as<int32_t>() + e0, (e1 - e0), ncclInt32, s.peer, ctx->comm, st));
@@ -235,7 +273,7 @@ static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<in
             AFSAI_NCCL_TRY(ncclSend(X->b_col.as<int32_t>() + e0, (e1 - e0), ncclInt32, s.peer, ctx->comm, st));
             AFSAI_NCCL_TRY(ncclSend(X->b_val.as<double>() + e0, (e1 - e0), ncclDouble, s.peer, ctx->comm, st));
         }
-        AFSAI_NCCL_TRY(ncclGroupEnd());
+        AFSAI_NCCL_TRY(grp.end());
     }
     return AFSAI_OK;
 }
@@ -311,11 +349,12 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
     AFSAI_CUDA_TRY(cudaMemcpyAsync(dcnt.p, scnt.data(), np * 8, cudaMemcpyHostToDevice, st));
     {
         KTimer kt(ctx, AFSAI_K_COMM);
-        AFSAI_NCCL_TRY(ncclGroupStart());
+        NcclGroup grp;
+        AFSAI_NCCL_TRY(grp.start());
         for (int q = 0; q < me; ++q) AFSAI_NCCL_TRY(ncclSend(dcnt.as<int64_t>() + q, 1, ncclInt64, q, ctx->comm, st));
         for (int q = me + 1; q < np; ++q)
             AFSAI_NCCL_TRY(ncclRecv(dcnt.as<int64_t>() + np + q, 1, ncclInt64, q, ctx->comm, st));
-        AFSAI_NCCL_TRY(ncclGroupEnd());
+        AFSAI_NCCL_TRY(grp.end());
     }
     std::vector<int64_t> rcnt(np, 0), hall(2 * np);
     AFSAI_CUDA_TRY(cudaMemcpyAsync(hall.data(), dcnt.p, 2 * np * 8, cudaMemcpyDeviceToHost, st));
@@ -333,7 +372,8 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
     AFSAI_CUDA_TRY(rv_.alloc(std::max<int64_t>(total_r, 1) * 8, st));
     {
         KTimer kt(ctx, AFSAI_K_COMM);
-        AFSAI_NCCL_TRY(ncclGroupStart());
+        NcclGroup grp;
+        AFSAI_NCCL_TRY(grp.start());
         for (int q = 0; q < me; ++q)
             if (scnt[q] > 0) {
                 AFSAI_NCCL_TRY(ncclSend(sc[q].p, scnt[q], ncclInt32, q, ctx->comm, st));
@@ -346,7 +386,7 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
                 AFSAI_NCCL_TRY(ncclRecv(rr_.as<int32_t>() + rbase[q], rcnt[q], ncclInt32, q, ctx->comm, st));
                 AFSAI_NCCL_TRY(ncclRecv(rv_.as<double>() + rbase[q], rcnt[q], ncclDouble, q, ctx->comm, st));
             }
-        AFSAI_NCCL_TRY(ncclGroupEnd());
+        AFSAI_NCCL_TRY(grp.end());
     }
     dt.mark("exchange");
     // ---- local G^T rows [b, e): local entries + received triples
@@ -380,10 +420,10 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
                                                  n_out, F->t_rowptr.as<int64_t>(), cnt.as<int32_t>(),
                                                  tcol.as<int32_t>(), tval.as<double>());
     dt.mark("scatter");
-    sort_rows_kernel<<<grid, 256, 0, st>>>(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(),
-                                           F->t_col.as<int32_t>(), F->t_val.as<double>());
+    sort_gt_rows(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(), F->t_col.as<int32_t>(),
+                 F->t_val.as<double>(), grid, st, &ctx->launches);
     dt.mark("sort");
-    ctx->launches += 3;
+    ctx->launches += 2;
     AFSAI_CUDA_TRY(cudaGetLastError());
     return AFSAI_OK;
 }
@@ -392,7 +432,7 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
                afsai_status_t *status) {
     cudaStream_t st = ctx->stream;
     DeviceCsr A;
-    int rc = stage_csr(ctx, Ain, &A, status);
+    int rc = agree(ctx, stage_csr(ctx, Ain, &A, status), status);
     if (rc) return rc;
     auto *F = new afsai_factor_s();
     F->ctx = ctx;
@@ -413,14 +453,19 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
     if (rc) return fail(rc);
     D->bounds.assign(begins.begin(), begins.end());
     D->bounds.push_back(A.n_cols);
+    // every rank sees the same bounds, so these two checks agree by themselves
+    if (D->bounds[0] != 0)
+        return fail(set_status(status, AFSAI_EINVAL, "rank 0's block must start at row 0"));
     for (int q = 0; q < ctx->nranks; ++q)
         if (D->bounds[q + 1] < D->bounds[q])
             return fail(set_status(status, AFSAI_EINVAL, "row blocks must be contiguous in rank order"));
-    if (D->bounds[ctx->rank + 1] != A.row_begin + A.n_rows)
-        return fail(set_status(status, AFSAI_EINVAL, "row blocks must tile [0, n) in rank order"));
+    rc = D->bounds[ctx->rank + 1] != A.row_begin + A.n_rows
+             ? set_status(status, AFSAI_EINVAL, "row blocks must tile [0, n) in rank order")
+             : AFSAI_OK;
+    if ((rc = agree(ctx, rc, status))) return fail(rc);
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
     int64_t maxlen = 0;
-    rc = validate_csr(ctx, A, &maxlen, status);
+    rc = agree(ctx, validate_csr(ctx, A, &maxlen, status), status);
     if (rc) return fail(rc);
     rc = allreduce_max(ctx, maxlen, &maxlen, status);  // same kernel plan on every rank
     if (rc) return fail(rc);
@@ -442,7 +487,7 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
     const int64_t lo = b - reach;
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
     DeviceCsr X;
-    rc = gather_halo(ctx, A, D->bounds, lo, &X, status);
+    rc = agree(ctx, gather_halo(ctx, A, D->bounds, lo, &X, status), status);
     if (rc) return fail(rc);
 #ifdef AFSAI_BOUNDS_CHECK
     {   // debug build: the gathered halo-extended matrix must be a valid CSR
@@ -457,10 +502,10 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
 #endif
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
     F->stats.halo_rows = (int32_t)(b - lo);
-    rc = block_rows_to_G(ctx, X, lo, e, b, A.n_rows, p, maxlen, F, status);
+    rc = agree(ctx, block_rows_to_G(ctx, X, lo, e, b, A.n_rows, p, maxlen, F, status), status);
     if (rc) return fail(rc);
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
-    rc = dist_transpose(ctx, F, D->bounds, status);
+    rc = agree(ctx, dist_transpose(ctx, F, D->bounds, status), status);
     if (rc) return fail(rc);
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
     // G's lower reach (for the r halo of G r and the t halo of G^T t)
@@ -803,6 +848,7 @@ int afsai_setup_block(afsai_ctx_t ctx, const afsai_csr_t *Ain, int64_t row_lo, i
     F->n_global = Ain->n_cols;
     F->row_begin = row_lo;
     F->stats.n_rows = n_rows;
+    F->block = true;
     rc = block_rows_to_G(ctx, A, a_lo, a_hi, row_lo, n_rows, p, maxlen, F, status);
     if (rc) {
         delete F;

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -55,11 +56,18 @@ int stage_csr(afsai_ctx_t ctx, const afsai_csr_t *A, DeviceCsr *out, afsai_statu
         out->col = A->col;
         out->val = A->val;
         out->staged = false;
-        // base = rowptr[0] (read back; one tiny copy)
+        // base = rowptr[0] and the end offset (read back; two tiny copies)
+        int64_t last = 0;
         AFSAI_CUDA_TRY(cudaMemcpyAsync(&out->base, A->rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(&last, A->rowptr + A->n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                       ctx->stream));
         AFSAI_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (last - out->base != A->nnz)
+            return set_status(status, AFSAI_EINVAL, "rowptr[n_rows] - rowptr[0] != nnz");
         return AFSAI_OK;
     }
+    if (A->rowptr[A->n_rows] - A->rowptr[0] != A->nnz)
+        return set_status(status, AFSAI_EINVAL, "rowptr[n_rows] - rowptr[0] != nnz");
     out->base = A->rowptr[0];
     out->staged = true;
     AFSAI_CUDA_TRY(out->b_rowptr.alloc((A->n_rows + 1) * sizeof(int64_t), ctx->stream));
@@ -364,6 +372,52 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
 
 }  // namespace afsai
 
+// One library-owned pool per device, shared by the contexts on that device and
+// trimmed to zero when the last of them is destroyed (the device's default pool,
+// which other libraries use, is left alone).
+namespace {
+constexpr int kMaxDev = 64;
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[kMaxDev] = {};
+int g_pool_refs[kMaxDev] = {};
+}  // namespace
+
+namespace afsai {
+cudaMemPool_t library_pool() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDev) return nullptr;
+    return g_pool[d];
+}
+}  // namespace afsai
+
+static cudaMemPool_t pool_acquire(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= kMaxDev) return nullptr;
+    if (!g_pool[dev]) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.handleTypes = cudaMemHandleTypeNone;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = dev;
+        if (cudaMemPoolCreate(&g_pool[dev], &pp) != cudaSuccess) {
+            cudaGetLastError();
+            g_pool[dev] = nullptr;
+            return nullptr;
+        }
+    }
+    ++g_pool_refs[dev];
+    return g_pool[dev];
+}
+
+static void pool_release(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= kMaxDev || !g_pool[dev]) return;
+    if (--g_pool_refs[dev] <= 0) {
+        g_pool_refs[dev] = 0;
+        cudaMemPoolTrimTo(g_pool[dev], 0);  // return every unused byte to the device
+    }
+}
+
 using namespace afsai;
 
 extern "C" {
@@ -386,10 +440,12 @@ const char *afsai_strerror(int code) {
 
 static int ctx_init(afsai_ctx_t c, void *stream, afsai_status_t *status) {
     AFSAI_CUDA_TRY(cudaGetDevice(&c->device));
-    // keep freed stream-ordered allocations cached in the device pool: the set-up
-    // scratch and G are re-allocated every call and remapping them costs ms
-    cudaMemPool_t pool;
-    if (std::getenv("AFSAI_POOL_KEEP0") == nullptr && cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+    // keep freed stream-ordered allocations cached in the library pool while a
+    // context lives: the set-up scratch and G are re-allocated every call and
+    // remapping them costs ms
+    cudaMemPool_t pool = pool_acquire(c->device);
+    c->pool_held = pool != nullptr;
+    if (pool) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         // Map device memory into the pool once (default 20% of the device, at most half
@@ -403,7 +459,7 @@ static int ctx_init(afsai_ctx_t c, void *stream, afsai_status_t *status) {
         if (const char *e = std::getenv("AFSAI_POOL_PREWARM_GB")) gb = std::atof(e);
         if (gb > 0) {
             void *p = nullptr;
-            if (cudaMallocAsync(&p, (size_t)(gb * 1073741824.0), (cudaStream_t)stream) == cudaSuccess) {
+            if (cudaMallocFromPoolAsync(&p, (size_t)(gb * 1073741824.0), pool, (cudaStream_t)stream) == cudaSuccess) {
                 cudaFreeAsync(p, (cudaStream_t)stream);
                 cudaStreamSynchronize((cudaStream_t)stream);
             } else {
@@ -479,6 +535,7 @@ void afsai_ctx_destroy(afsai_ctx_t ctx) {
         cudaEventDestroy(t.b);
     }
     for (auto e : ctx->pool) cudaEventDestroy(e);
+    if (ctx->pool_held) pool_release(ctx->device);
     delete ctx;
 }
 
@@ -703,9 +760,9 @@ int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out
                                            F->g_val.as<double>(), F->row_begin, col_lo, n_out,
                                            F->t_rowptr.as<int64_t>(), cnt.as<int32_t>(), tcol.as<int32_t>(),
                                            tval.as<double>());
-    sort_rows_kernel<<<grid, 256, 0, st>>>(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(),
-                                           F->t_col.as<int32_t>(), F->t_val.as<double>());
-    ctx->launches += 2;
+    sort_gt_rows(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(), F->t_col.as<int32_t>(),
+                 F->t_val.as<double>(), grid, st, &ctx->launches);
+    ctx->launches += 1;
     AFSAI_CUDA_TRY(cudaGetLastError());
     return AFSAI_OK;
 }
@@ -771,6 +828,7 @@ extern "C" {
 int afsai_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z) {
     afsai_status_t *status = nullptr;
     if (!ctx || !F || !r || !z || r == z) return AFSAI_EINVAL;
+    if (F->ctx != ctx || F->block) return AFSAI_EINVAL;  // another context's factor / a block factor (no G^T)
     if (ctx->nranks > 1) return dist_apply(ctx, F, r, z, status);
     const int64_t n = F->n_rows;
     cudaStream_t st = ctx->stream;
@@ -802,6 +860,8 @@ int afsai_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const d
     set_status(status, AFSAI_OK, "");
     if (!ctx || !Ain || !F || !b || !x || !(tol > 0.0) || max_iters < 1)
         return set_status(status, AFSAI_EINVAL, "bad PCG arguments");
+    if (F->ctx != ctx || F->block)
+        return set_status(status, AFSAI_EINVAL, "factor belongs to another context or is a block factor (no G^T)");
     if (Ain->n_rows != F->n_rows || Ain->row_begin != F->row_begin)
         return set_status(status, AFSAI_EINVAL, "A does not match the factor's rows");
     if (ctx->nranks > 1) return dist_pcg(ctx, Ain, F, b, x, tol, max_iters, rep, status);
@@ -931,7 +991,7 @@ int afsai_factor_nnz(afsai_factor_t F, int64_t *nnz_G, int64_t *nnz_Gt) {
 
 int afsai_factor_copy(afsai_factor_t F, int32_t which, int64_t *rowptr, int32_t *col, double *val) {
     afsai_status_t *status = nullptr;
-    if (!F || (which != 0 && which != 1)) return AFSAI_EINVAL;
+    if (!F || (which != 0 && which != 1) || (which == 1 && F->block)) return AFSAI_EINVAL;
     cudaStream_t st = F->ctx->stream;
     const int64_t n = F->n_rows, nnz = which ? F->nnz_Gt : F->nnz_G;
     const DevBuf &rp = which ? F->t_rowptr : F->g_rowptr;

@@ -1,6 +1,9 @@
 // setup_common.cuh -- device code shared by the two per-row set-up kernels
 // (setup_scan.cu: general rows; setup_hits.cu: short rows with hit lists).
 #pragma once
+#ifndef AFSAI_FMAD_OFF
+#error "set-up device code must be compiled with -fmad=false -DAFSAI_FMAD_OFF (arithmetic contract, DESIGN.md 3.1)"
+#endif
 #include <cuda_runtime.h>
 
 #include <cstdint>
