@@ -231,7 +231,26 @@ def fe_elasticity(N: int, nu: float = 0.3, hetero: bool = True) -> CSR:
     N x N x N free nodes (the z = 0 plane is clamped and eliminated), 3 dof/node,
     node-major, x fastest; per-element log10 E ~ U(-1, 1).  Couplings summed in
     ascending element order, then the strictly-upper part is mirrored from the lower."""
-    return fe_elasticity_rows(N, 0, 3 * N * N * N, nu, hetero)
+    n = 3 * N * N * N
+    step = 3 * N * N * max(1, 2_000_000 // (3 * N * N))   # whole node planes, ~2M rows per slab
+    if n <= step:
+        return fe_elasticity_rows(N, 0, n, nu, hetero)
+    # large N (M5): slabs of rows (bitwise the full matrix's rows), concatenated;
+    # bounded peak memory instead of the (n/3) x 27 x 3 x 3 block array at once
+    parts = [fe_elasticity_rows(N, a, min(n, a + step), nu, hetero) for a in range(0, n, step)]
+    nnz = sum(p.nnz for p in parts)
+    rowptr = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    r = e = 0
+    rowptr[0] = 0
+    for p in parts:
+        rowptr[r + 1: r + p.n + 1] = p.rowptr[1:] + e
+        col[e: e + p.nnz] = p.col
+        val[e: e + p.nnz] = p.val
+        r += p.n
+        e += p.nnz
+    return CSR(n, rowptr, col, val, f"fe_{N}")
 
 
 def fe_elasticity_rows(N: int, row_lo: int, row_hi: int, nu: float = 0.3, hetero: bool = True) -> CSR:
@@ -340,6 +359,36 @@ def random_sparse_spd(n: int, nnz_per_row: int = 6, sub: int = 0, bandwidth: int
     A.sort_indices()
     return CSR(n, A.indptr.astype(np.int64), A.indices.astype(np.int32), A.data.astype(np.float64),
                f"rsparse{n}_{sub}")
+
+
+def arrow_spd(n: int) -> CSR:
+    """Tridiagonal 1D Laplacian plus a hub: row/column 0 coupled to every row
+    (a_0j = a_j0 = -0.5 / n^0.5).  Every row's pattern can select column 0, so
+    G^T's row 0 is about n long (exercises the long-row transpose path).
+    Strictly diagonally dominant, hence SPD; bitwise symmetric by construction."""
+    c = -0.5 / np.sqrt(n)
+    d = np.full(n, 3.0)
+    d[0] = 2.0 + (n - 1) * abs(c)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        cs = {i: d[i]}
+        if i > 0:
+            cs[0] = c if i > 1 else c - 1.0
+            cs[i - 1] = cs.get(i - 1, 0.0) + (-1.0 if i > 1 else 0.0)
+        if i < n - 1:
+            cs[i + 1] = cs.get(i + 1, 0.0) + (-1.0 if i + 1 > 1 else 0.0)
+        if i == 0:
+            for j in range(1, n):
+                cs[j] = c if j > 1 else c - 1.0
+        for j in sorted(cs):
+            rows.append(i)
+            cols.append(j)
+            vals.append(cs[j])
+    rows = np.asarray(rows)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rowptr, rows + 1, 1)
+    np.cumsum(rowptr, out=rowptr)
+    return CSR(n, rowptr, np.asarray(cols, dtype=np.int32), np.asarray(vals, dtype=np.float64), f"arrow{n}")
 
 
 def diagonal(d) -> CSR:

@@ -1,16 +1,19 @@
 #!/usr/bin/env python3
-"""bench.py -- aFSAI set-up + PCG on B200 (driver contract, see DESIGN.md §7).
+"""bench.py -- aFSAI set-up + PCG on B200 (driver contract, see DESIGN.md §5).
 
-One step = one pass of the whole hot path on the
-BASELINE.json configs[1] workload (M2: 3D 7-point Poisson 100^3, aFSAI 20 x 2,
-PCG to 1e-8): afsai_setup (validate, per-row set-up kernel, assembly, G^T)
-followed by afsai_pcg from x0 = 0 to ||r||/||b|| <= 1e-8.
-value = nnz(G) / (T_setup + T_solve), whole job over all ranks.
+One step = one pass of the whole hot path: afsai_setup
+(validate, per-row set-up kernel, assembly, G^T) followed by afsai_pcg from
+x0 = 0 to ||r||/||b|| <= 1e-8, on device-resident A and b.
+value = nnz(G) / (T_setup + T_solve), whole job over all ranks (G-nnz/s).
 
-N > 1 (torchrun, one process per GPU): weak scaling -- rank p owns the slab
-z in [100p, 100p+100) of a 100 x 100 x (100 N) Poisson grid (the paper's weak
-scaling experiment, at 10^6 rows per GPU); the set-up halo and the
-per-iteration halos / all-reduces go over NCCL.
+Default workload: M3 = BASELINE.json configs[2], the config the metric's
+"at 1/2/4/8 B200" is quoted on (3D heterogeneous/anisotropic Poisson 200^3,
+8M rows, aFSAI 20 x 2).  N > 1 (torchrun, one process per GPU): STRONG scaling
+of the same matrix -- rank p owns rows [p n/N, (p+1) n/N); the exact set-up
+halo, the G^T exchange and the per-iteration halos / all-reduces go over NCCL.
+--workload M2|M4|M5 picks another config; --weak runs the round-1 weak-scaling
+experiment (rank p owns a 100^3 slab of a 100 x 100 x 100N Poisson grid,
+P:1183-1205).
 
 --impl reference: the CPU oracle (oracle/), as it stands, on the host cores,
 on a bounded slab of the same workload; rank 0 only.
@@ -30,9 +33,14 @@ sys.path.insert(0, ROOT)
 
 METRIC = "aFSAI set-up time & G-nnz/s at 1/2/4/8 B200; PCG iters and solve time"
 UNIT = "G-nnz/s"
-NX = 100            # per-rank slab: NX x NX x NX rows
-NSTEPS, S, EPS, CAP = 20, 2, 0.0, 1000
+NX = 100            # --weak: per-rank slab NX x NX x NX rows
 TOL = 1e-8
+
+
+def workload_params(name):
+    import afsai_inputs as ai
+    c = ai.CONFIGS[name]
+    return c["nsteps"], c["s"], c["eps"], c["max_row_nnz"]
 
 
 def parse():
@@ -42,6 +50,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=NX)
+    ap.add_argument("--workload", default="M3", choices=["M2", "M3", "M4", "M5"])
+    ap.add_argument("--weak", action="store_true", help="round-1 weak scaling: a 100^3 Poisson slab per GPU")
+    ap.add_argument("--e2e-runs", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -120,63 +131,82 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- reference arm (oracle)
+def oracle_sample(args):
+    """A bounded sample of the workload for the CPU oracle (~10-30 s of CPU work on
+    the box's cores): a slab of the same generator with the same aFSAI parameters."""
+    import afsai_inputs as ai
+    cores = os.cpu_count() or 1
+    w = "M2" if args.weak else args.workload
+    if w == "M2":
+        nz = max(2, min(args.nx, int(round(40 * cores / 8))))
+        A, label = ai.poisson3d(args.nx, args.nx, nz), f"Poisson {args.nx}x{args.nx}x{nz} slab of M2"
+    elif w == "M3":
+        nz = max(2, min(200, int(round(2 * cores))))
+        A, label = ai.hetero_poisson3d(200, 200, nz), f"heterogeneous Poisson 200x200x{nz} slab of M3"
+    else:
+        N = max(8, int(round((cores * 15 / 1.5e-3 / 3) ** (1 / 3))))
+        A, label = ai.fe_elasticity(N), f"FE elasticity {N}^3 nodes (M4/M5 generator)"
+    return A, label, workload_params(w), cores
+
+
+def run_oracle_step(A, b, prm, cores):
+    import oracle
+    k, s, eps, cap = prm
+    G, Gt, _ = oracle.setup_full(A, k, s, eps, cap, threads=cores)
+    r = oracle.pcg(A, G, Gt, b, tol=TOL, max_iters=20000)
+    return G.nnz, r.iters
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     import numpy as np
 
     import afsai_inputs as ai
-    import oracle
-    cores = os.cpu_count() or 1
-    # bounded slab of the workload: NX x NX x nz, nz sized so each step is ~10-30 s of CPU
-    nz = max(2, min(args.nx, int(round(40 * cores / 8))))
-    A = ai.poisson3d(args.nx, args.nx, nz)
+    A, label, prm, cores = oracle_sample(args)
     b, _ = ai.rhs_for(A)
     times = []
     nnzG = iters = 0
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        G, Gt, _ = oracle.setup_full(A, NSTEPS, S, EPS, CAP, threads=cores)
-        r = oracle.pcg(A, G, Gt, b, tol=TOL)
+        nnzG, iters = run_oracle_step(A, b, prm, cores)
         t1 = time.perf_counter()
         if k >= args.warmup:
             times.append(t1 - t0)
-        nnzG, iters = G.nnz, r.iters
         if k == 0 and args.warmup + args.steps > 2 and (t1 - t0) * (args.warmup + args.steps) > 240:
             args.warmup, args.steps = 0, 1   # keep the run within minutes
             times = [t1 - t0]
             break
     ms = 1e3 * float(np.mean(times))
     value = nnzG / (ms * 1e-3)
-    sample = (f"Poisson {args.nx}x{args.nx}x{nz} slab of M2 ({A.n} rows, nnz(G)={nnzG}): oracle set-up "
-              f"(aFSAI {NSTEPS}x{S}) + oracle PCG to {TOL} ({iters} iters) per step")
+    sample = (f"{label} ({A.n} rows, nnz(G)={nnzG}): oracle set-up (aFSAI {prm[0]}x{prm[1]}, {cores} threads) "
+              f"+ oracle PCG to {TOL} ({iters} iters) per step")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": len(times), "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"M2 slab {args.nx}x{args.nx}x{nz} (CPU oracle)", "nsteps": NSTEPS, "s": S,
-                       "eps": EPS, "pcg_tol": TOL},
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{label} (CPU oracle)", "nsteps": prm[0], "s": prm[1], "eps": prm[2],
+                       "max_row_nnz": prm[3], "pcg_tol": TOL},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_leg(args):
-    """The oracle as it stands, on the host cores, on a bounded slab (~10-30 s)."""
+    """The oracle as it stands, on the host cores, on a bounded sample (~10-30 s)."""
     import afsai_inputs as ai
     import oracle
-    cores = os.cpu_count() or 1
-    nz = max(2, min(args.nx, int(round(40 * cores / 8))))   # ~10-30 s of CPU work
-    A = ai.poisson3d(args.nx, args.nx, nz)
+    A, label, prm, cores = oracle_sample(args)
     b, _ = ai.rhs_for(A)
+    k, s, eps, cap = prm
     t0 = time.perf_counter()
-    G, Gt, _ = oracle.setup_full(A, NSTEPS, S, EPS, CAP, threads=cores)
+    G, Gt, _ = oracle.setup_full(A, k, s, eps, cap, threads=cores)
     t1 = time.perf_counter()
-    r = oracle.pcg(A, G, Gt, b, tol=TOL)
+    r = oracle.pcg(A, G, Gt, b, tol=TOL, max_iters=20000)
     t2 = time.perf_counter()
     value = G.nnz / (t2 - t0)
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"Poisson {args.nx}x{args.nx}x{nz} slab of M2 ({A.n} rows): oracle set-up {t1 - t0:.2f} s "
-                      f"({cores} threads) + sequential oracle PCG {t2 - t1:.2f} s ({r.iters} iters)",
+            "sample": f"{label} ({A.n} rows): oracle set-up {t1 - t0:.2f} s ({cores} threads) + sequential "
+                      f"oracle PCG {t2 - t1:.2f} s ({r.iters} iters)",
             "setup_s": t1 - t0, "pcg_s": t2 - t1, "pcg_iters": r.iters}
 
 
@@ -201,11 +231,20 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nx = args.nx
-    # global problem: nx x nx x (nx * world); this rank owns rows of its slab
-    n_loc = nx * nx * nx
-    Aglob = ai.poisson3d(nx, nx, nx * world) if world > 1 else ai.poisson3d(nx)
+    if args.weak:
+        # global problem: nx x nx x (nx * world); this rank owns rows of its slab
+        wname = "M2"
+        n_loc = nx * nx * nx
+        Aglob = ai.poisson3d(nx, nx, nx * world) if world > 1 else ai.poisson3d(nx)
+        row_begin = rank * n_loc
+    else:
+        # strong scaling: the BASELINE.json config, rank p owns rows [p n / N, (p+1) n / N)
+        wname = args.workload
+        Aglob = ai.CONFIGS[wname]["make"]()
+        row_begin = rank * Aglob.n // world
+        n_loc = (rank + 1) * Aglob.n // world - row_begin
+    NSTEPS, S, EPS, CAP = workload_params(wname)
     b_glob, _ = ai.rhs_for(Aglob)
-    row_begin = rank * n_loc
     dA = DeviceCSR.from_numpy(Aglob, row_begin=row_begin, n_rows=n_loc)
     b = torch.from_numpy(np.ascontiguousarray(b_glob[row_begin: row_begin + n_loc])).cuda()
     x = torch.empty_like(b)
@@ -286,20 +325,27 @@ def main():
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     fp64_peak_tf = nsm * 64 * 2 * sm_max * 1e6 / 1e12
     setup_flop = 2.0 * (stats["fma_border"] + stats["fma_backsub"] + stats["fma_grad"])
+    dfma_probe_tf = ctx.dfma_peak()[0] / 1e12
     per_class = {k: {"launches": v[0] // args.steps, "ms_per_step": v[1] / args.steps} for k, v in ktimes.items()}
     solve_kernels_ms = (ms_G + ms_T + ktimes["spmv_A"][1] + ktimes["vector"][1]) / args.steps
     if setup_ms >= max(ms_G, ms_T) / args.steps:
         achieved = setup_flop / (setup_ms * 1e-3) / 1e12
         # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-        traffic = None
+        traffic, tfile = None, f"r02_setup_traffic_{wname}.json"
         try:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_setup_traffic.json")))["dram_bytes_per_launch"]
+            traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))["dram_bytes_per_launch"]
         except Exception:
             pass
-        roof = {"kernel": "afsai_setup_rows_lockstep_kernel<16, 3, 2, 6>", "bound": "alu", "achieved": achieved,
+        from paper_2010_14175_b200.capi import afsai_setup_stats_t
+        plan = afsai_setup_stats_t.PLANS.get(stats["plan"], "?")
+        roof = {"kernel": f"afsai_setup_rows_{plan}_kernel (lanes/row {stats['lanes_per_row']}, "
+                          f"table {stats['table_size']}, {stats['rows_per_cta']} rows/CTA)",
+                "bound": "alu", "achieved": achieved,
                 "peak": fp64_peak_tf, "unit": "TFLOP/s", "frac": achieved / fp64_peak_tf, "traffic": traffic,
-                "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r01_setup_traffic.json)",
-                "peak_source": f"{nsm} SM x 64 DFMA/clk x 2 x {sm_max:.0f} MHz (unit counts, DESIGN.md §5)",
+                "traffic_unit": f"bytes per launch (dram read + write, ncu --set full, profiles/{tfile})",
+                "peak_source": (f"{nsm} SM x 64 DFMA/clk x 2 x {sm_max:.0f} MHz (unit counts, B200_PROFILING.md; "
+                                f"MEASURED_PEAKS.json has no fp64 entry); in-run DFMA probe "
+                                f"{dfma_probe_tf:.1f} TF/s (afsai_probe_dfma_peak)"),
                 "algorithmic_flop_per_launch": setup_flop, "avg_launch_ms": setup_ms}
     else:
         avg = ms_G / max(la_G, 1)
@@ -344,7 +390,7 @@ def main():
         h2d = hA.rowptr.numel() * 8 + hA.col.numel() * 4 + hA.val.numel() * 8 + hb.numel() * 8
         d2h = hx.numel() * 8
         e_ms = []
-        for k in range(2):
+        for k in range(args.e2e_runs + 1):   # one warm-up (host staging buffers, pinned paths), then runs
             flush.zero_()
             torch.cuda.synchronize()
             barrier()
@@ -355,15 +401,16 @@ def main():
             t1 = time.perf_counter()
             F.close()
             e_ms.append((t1 - t0) * 1e3)
-        em = min(e_ms[1:] or e_ms)
+        em = float(np.median(e_ms[1:] or e_ms))
         if world > 1:
             import torch.distributed as dist
             t = torch.tensor([em], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             em = float(t[0])
         e2e = {"value": nnz_total / (em * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": em,
-               "timing": "host wall clock around afsai_setup(host A) + afsai_pcg(host b -> host x)"}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": em, "runs_ms": e_ms[1:],
+               "timing": f"median of {len(e_ms) - 1} runs, host wall clock around afsai_setup(host A) + "
+                         f"afsai_pcg(host b -> host x), max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -372,10 +419,12 @@ def main():
     if rank == 0:
         clocks = clk.summary()
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+                "scaling": "weak" if args.weak else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"M2: 3D 7-point Poisson {nx}^3 per GPU (global {nx}x{nx}x{nx * world}), "
-                                       f"aFSAI {NSTEPS}x{S}, PCG to {TOL}",
+                "config": {"workload": (f"M2 weak scaling: 3D 7-point Poisson {nx}^3 per GPU (global "
+                                        f"{nx}x{nx}x{nx * world}), aFSAI {NSTEPS}x{S}, PCG to {TOL}") if args.weak
+                           else f"{wname}: {ai.CONFIGS[wname]['desc']}, PCG to {TOL}, rows split over {world} GPU(s)",
                            "global_rows": Aglob.n, "nnz_A": Aglob.nnz, "nsteps": NSTEPS, "s": S, "eps": EPS,
                            "max_row_nnz": CAP, "pcg_tol": TOL, "parallelism": f"rows{world}",
                            "l2": "flushed (256 MiB write) between timed steps; A+G+scratch > 126 MB L2"},

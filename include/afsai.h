@@ -114,7 +114,15 @@ typedef struct {
     int64_t phase_cycles[7];     /* SM cycles summed over warps in the set-up kernel:
                                     prologue, gradient, select, gather, border, backsub, output */
     int64_t max_universe;        /* largest candidate+pattern set of a row (table keys) */
+    int32_t plan;                /* kernel plan of the main pass: AFSAI_PLAN_*        */
+    int32_t lanes_per_row;       /* lanes of a warp working on one row               */
+    int32_t value_bytes;         /* 8: fp64 set-up; 4: fp32 set-up (AFSAI_SETUP_FP32) */
+    int32_t reserved;
 } afsai_setup_stats_t;
+#define AFSAI_PLAN_LOCKSTEP 0    /* hit lists, several rows per warp in lockstep (stencils) */
+#define AFSAI_PLAN_PROW 1        /* pattern-row folds (long rows, FE)                        */
+#define AFSAI_PLAN_HITS 2        /* hit lists, one row per lane group                        */
+#define AFSAI_PLAN_SCAN 3        /* general: candidate rows re-read every step               */
 
 typedef struct {
     int32_t iters;               /* PCG iterations performed                          */
@@ -188,6 +196,11 @@ int afsai_factor_copy(afsai_factor_t F, int32_t which, int64_t *rowptr, int32_t 
 /* Per-row trace: steps taken and stop reason (int32 n_rows each; host or device). */
 int afsai_factor_trace(afsai_factor_t F, int32_t *steps, int32_t *reason);
 int afsai_factor_stats(afsai_factor_t F, afsai_setup_stats_t *stats);
+/* Rows whose on-chip candidate tables overflowed in the first pass of the set-up
+ * kernel and were recomputed by a retry pass with larger tables:
+ * *count = their number (always set); the first min(count, max_rows) global row
+ * indices (unordered) are copied into rows (host or device; may be NULL). */
+int afsai_factor_retried(afsai_factor_t F, int64_t *rows, int64_t max_rows, int64_t *count);
 void afsai_factor_destroy(afsai_factor_t F);
 
 /* ---- instrumentation for bench/tests: number of kernels this library has

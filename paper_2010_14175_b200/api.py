@@ -126,6 +126,15 @@ class Factor:
         capi.afsai_factor_trace(self.h, st, rs)
         return st, rs
 
+    def retried_rows(self):
+        """Global rows the set-up recomputed with larger on-chip tables (sorted, int64 numpy)."""
+        import numpy as np
+        k = capi.afsai_factor_retried(self.h)
+        rows = torch.empty(max(k, 1), dtype=torch.int64)
+        if k:
+            capi.afsai_factor_retried(self.h, rows)
+        return np.sort(rows[:k].numpy())
+
     def stats(self) -> dict:
         return capi.afsai_factor_stats(self.h).to_dict()
 

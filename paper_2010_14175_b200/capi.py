@@ -24,7 +24,7 @@ STOP_NAMES = {0: "kmax", 1: "cap", 2: "no_candidates", 3: "tolerance"}
 EXPORTS = [
     "afsai_version", "afsai_strerror", "afsai_ctx_create", "afsai_nccl_unique_id", "afsai_ctx_create_nccl",
     "afsai_ctx_rank", "afsai_ctx_destroy", "afsai_setup", "afsai_apply", "afsai_pcg", "afsai_factor_nnz",
-    "afsai_factor_copy", "afsai_factor_trace", "afsai_factor_stats", "afsai_factor_destroy",
+    "afsai_factor_copy", "afsai_factor_trace", "afsai_factor_stats", "afsai_factor_retried", "afsai_factor_destroy",
     "afsai_ctx_launches", "afsai_probe_dfma_peak", "afsai_ctx_set_timing", "afsai_ctx_kernel_times",
     "afsai_setup_block", "afsai_plan_ranges",
 ]
@@ -55,7 +55,9 @@ class afsai_setup_stats_t(ctypes.Structure):
                 ("ms_assemble", ctypes.c_double), ("ms_transpose", ctypes.c_double), ("ms_halo", ctypes.c_double),
                 ("table_size", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32), ("retried_rows", ctypes.c_int32),
                 ("halo_rows", ctypes.c_int32), ("phase_cycles", ctypes.c_int64 * 7),
-                ("max_universe", ctypes.c_int64)]
+                ("max_universe", ctypes.c_int64), ("plan", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
+                ("value_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+    PLANS = {0: "lockstep", 1: "prow", 2: "hits", 3: "scan"}
 
     PHASES = ["prologue", "gradient", "select", "gather", "border", "backsub", "output"]
 
@@ -97,6 +99,7 @@ def load_library(path: str = LIB_PATH):
         "afsai_factor_copy": ([P, i32, P, P, P], ctypes.c_int),
         "afsai_factor_trace": ([P, P, P], ctypes.c_int),
         "afsai_factor_stats": ([P, ctypes.POINTER(afsai_setup_stats_t)], ctypes.c_int),
+        "afsai_factor_retried": ([P, P, i64, P], ctypes.c_int),
         "afsai_factor_destroy": ([P], None),
         "afsai_ctx_launches": ([P], i64),
         "afsai_probe_dfma_peak": ([P, P, P], ctypes.c_int),
@@ -237,6 +240,16 @@ def afsai_factor_stats(F) -> afsai_setup_stats_t:
     if rc:
         raise AfsaiError(rc, where="afsai_factor_stats")
     return s
+
+
+def afsai_factor_retried(F, rows=None) -> int:
+    """Number of retried rows; with a (host or device) int64 tensor `rows`, also copies them."""
+    cnt = ctypes.c_int64()
+    mx = rows.numel() if rows is not None else 0
+    rc = lib().afsai_factor_retried(F, _ptr(rows) if rows is not None else None, mx, ctypes.byref(cnt))
+    if rc:
+        raise AfsaiError(rc, where="afsai_factor_retried")
+    return int(cnt.value)
 
 
 def afsai_factor_destroy(F):

@@ -98,6 +98,8 @@ struct DeviceCsr {
 // Scratch of one afsai_setup call.
 struct SetupWork {
     DevBuf scol, sval, nnz_row, err, retry, retry_count, work, counters;
+    DevBuf retried;          // global rows the first pass overflowed (recomputed with larger tables)
+    int64_t n_retried = 0;
     int32_t *steps = nullptr, *reason = nullptr;  // point into the factor
     int alloc(afsai_ctx_t ctx, int64_t n, int32_t mmax, afsai_status_t *status);
     int check_error(afsai_ctx_t ctx, afsai_status_t *status);
@@ -186,6 +188,8 @@ struct afsai_factor_s {
     int64_t nnz_Gt = 0;
     // per-row trace
     afsai::DevBuf steps, reason;
+    afsai::DevBuf retried;       // global rows recomputed by a retry pass (afsai_factor_retried)
+    int64_t n_retried = 0;
     afsai_setup_stats_t stats{};
     // multi-GPU: column reach of G below / above the local block (for halos)
     int64_t g_lo = 0;   // min column of G over local rows

@@ -194,6 +194,8 @@ int block_rows_to_G(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
     rc = W.read_stats(ctx, &F->stats, status);
     if (rc) return rc;
+    F->retried = std::move(W.retried);
+    F->n_retried = W.n_retried;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
     F->stats.ms_rows = ms;

@@ -279,6 +279,10 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         if (first) {
             stats->table_size = H;
             stats->rows_per_cta = rows_per_cta;
+            stats->plan = (hits && lockstep) ? AFSAI_PLAN_LOCKSTEP : prow ? AFSAI_PLAN_PROW
+                                                             : hits ? AFSAI_PLAN_HITS : AFSAI_PLAN_SCAN;
+            stats->lanes_per_row = lpr;
+            stats->value_bytes = 8;
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
@@ -344,6 +348,12 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         const int r = pass(rows, todo, &rc);
         if (r != AFSAI_OK) return r;
         todo = rc;
+        if (rc > 0 && rows == nullptr) {  // the first pass's overflow list: every retried row
+            AFSAI_CUDA_TRY(W.retried.alloc(rc * sizeof(int64_t), ctx->stream));
+            AFSAI_CUDA_TRY(cudaMemcpyAsync(W.retried.p, W.retry.p, rc * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
+            W.n_retried = rc;
+        }
         if (rc > 0) {
             retried_total += rc;
             AFSAI_CUDA_TRY(retry_in.alloc(rc * sizeof(int64_t), ctx->stream));
@@ -647,6 +657,8 @@ int local_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[4], st));
     rc = W.read_stats(ctx, &F->stats, status);
     if (rc) return fail(rc);
+    F->retried = std::move(W.retried);
+    F->n_retried = W.n_retried;
     F->stats.nnz_G = F->nnz_G;
     F->stats.nnz_Gt = F->nnz_Gt;
     F->stats.ms_total = elapsed(ctx->ev[1], ctx->ev[4]);
@@ -1013,6 +1025,18 @@ int afsai_factor_trace(afsai_factor_t F, int32_t *steps, int32_t *reason) {
     if (reason && F->n_rows)
         AFSAI_CUDA_TRY(cudaMemcpyAsync(reason, F->reason.p, F->n_rows * sizeof(int32_t), cudaMemcpyDefault, st));
     AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+    return AFSAI_OK;
+}
+
+int afsai_factor_retried(afsai_factor_t F, int64_t *rows, int64_t max_rows, int64_t *count) {
+    afsai_status_t *status = nullptr;
+    if (!F || !count || max_rows < 0) return AFSAI_EINVAL;
+    *count = F->n_retried;
+    const int64_t k = std::min(max_rows, F->n_retried);
+    if (rows && k > 0) {
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(rows, F->retried.p, k * sizeof(int64_t), cudaMemcpyDefault, F->ctx->stream));
+        AFSAI_CUDA_TRY(cudaStreamSynchronize(F->ctx->stream));
+    }
     return AFSAI_OK;
 }
 

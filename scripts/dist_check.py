@@ -1,9 +1,12 @@
-"""Multi-GPU checks under torchrun (one process per GPU, NCCL):
-  - G from the N-GPU set-up is bitwise the 1-GPU G (exact halo);
-  - G^T rows equal the 1-GPU G^T rows;
-  - afsai_apply equals the 1-GPU apply within the SpMV rounding bound;
-  - PCG iterations equal the 1-GPU count within 1.
-Each rank also runs the 1-GPU path on the whole (small) matrix for reference."""
+"""Multi-GPU parity under torchrun (one process per GPU, NCCL), against the CPU ORACLE:
+  - the local rows of G from the N-GPU set-up are bitwise the oracle's rows
+    (exact halo; row independence P:370-372);
+  - the local rows of G^T are bitwise the oracle transpose's rows (C10);
+  - afsai_apply matches oracle.apply within the SpMV rounding bound;
+  - PCG iterations within 1 of the oracle PCG (BASELINE.json north_star);
+  - error agreement: a matrix that is not SPD in the LAST rank's rows only makes
+    every rank return an error (no rank is left waiting in a collective).
+Prints one JSON document on rank 0 with "ok"."""
 import json
 import os
 import sys
@@ -14,6 +17,7 @@ import torch
 import torch.distributed as dist
 
 import afsai_inputs as ai
+import oracle
 from paper_2010_14175_b200 import capi
 from paper_2010_14175_b200.api import Context, DeviceCSR, Factor
 
@@ -25,57 +29,66 @@ results = {}
 cases = [("poisson3d_24", ai.poisson3d(24), 20, 2, 1000),
          ("hetero_16", ai.hetero_poisson3d(16), 20, 2, 1000),
          ("fe_7", ai.fe_elasticity(7), 30, 3, 100)]
+ctx = Context()
+u = 2.0 ** -53
 for name, A, k, s, cap in cases:
     n = A.n
     bounds = [n * q // world for q in range(world + 1)]
     b, e = bounds[rank], bounds[rank + 1]
-    # 1-GPU reference on this rank (non-NCCL context)
-    h1 = capi.afsai_ctx_create(torch.cuda.current_stream().cuda_stream)
-    Afull = DeviceCSR.from_numpy(A)
-    Afull_c = Afull.c()
-    F1 = capi.afsai_setup(h1, Afull_c, k, s, 0.0, cap)
-    nnz1, nnzt1 = capi.afsai_factor_nnz(F1)
-    g1 = [torch.empty(n + 1, dtype=torch.int64, device="cuda"), torch.empty(nnz1, dtype=torch.int32, device="cuda"),
-          torch.empty(nnz1, dtype=torch.float64, device="cuda")]
-    capi.afsai_factor_copy(F1, 0, *g1)
-    t1 = [torch.empty(n + 1, dtype=torch.int64, device="cuda"), torch.empty(nnzt1, dtype=torch.int32, device="cuda"),
-          torch.empty(nnzt1, dtype=torch.float64, device="cuda")]
-    capi.afsai_factor_copy(F1, 1, *t1)
+    # oracle: this rank's rows of G, the full G / G^T for apply and PCG
+    Gref, Tref, _ = oracle.setup_full(A, k, s, 0.0, cap)
     bvec, _ = ai.rhs_for(A)
-    rep1 = capi.afsai_pcg(h1, Afull_c, F1, torch.from_numpy(bvec).cuda(),
-                          torch.empty(n, dtype=torch.float64, device="cuda"), 1e-8, 5000)
-    r = torch.from_numpy(ai.rng("vectors", 21).standard_normal(n)).cuda()
-    z1 = torch.empty_like(r)
-    capi.afsai_apply(h1, F1, r, z1)
+    pr = oracle.pcg(A, Gref, Tref, bvec, tol=1e-8, max_iters=5000)
+    rv = ai.rng("vectors", 21).standard_normal(n)
+    zref = oracle.apply(Gref, Tref, rv)
     # N-GPU
-    ctx = Context()
     dA = DeviceCSR.from_numpy(A, row_begin=b, n_rows=e - b)
     F = Factor(ctx, dA, k, s, 0.0, cap)
-    rp, ci, v = F.G()
-    rp1 = g1[0][b:e + 1] - g1[0][b]
-    lo1, hi1 = int(g1[0][b]), int(g1[0][e])
-    ok_G = (torch.equal(rp, rp1) and torch.equal(ci, g1[1][lo1:hi1])
-            and torch.equal(v.view(torch.int64), g1[2][lo1:hi1].view(torch.int64)))
-    trp, tci, tv = F.Gt()
-    trp1 = t1[0][b:e + 1] - t1[0][b]
-    tl, th = int(t1[0][b]), int(t1[0][e])
-    ok_T = (torch.equal(trp, trp1) and torch.equal(tci, t1[1][tl:th])
-            and torch.equal(tv.view(torch.int64), t1[2][tl:th].view(torch.int64)))
-    z = F.apply(r[b:e].contiguous())
-    dz = (z - z1[b:e]).abs().max().item() / max(z1.abs().max().item(), 1e-300)
+    rp, ci, v = (t.cpu().numpy() for t in F.G())
+    a0, a1 = Gref.rowptr[b], Gref.rowptr[e]
+    ok_G = (np.array_equal(rp, Gref.rowptr[b:e + 1] - a0) and np.array_equal(ci, Gref.col[a0:a1])
+            and np.array_equal(v.view(np.int64), Gref.val[a0:a1].view(np.int64)))
+    trp, tci, tv = (t.cpu().numpy() for t in F.Gt())
+    t0, t1 = Tref.rowptr[b], Tref.rowptr[e]
+    ok_T = (np.array_equal(trp, Tref.rowptr[b:e + 1] - t0) and np.array_equal(tci, Tref.col[t0:t1])
+            and np.array_equal(tv.view(np.int64), Tref.val[t0:t1].view(np.int64)))
+    z = F.apply(torch.from_numpy(rv[b:e].copy()).cuda()).cpu().numpy()
+    bound = 2 * 64 * u * (abs(Tref.to_scipy()) @ (abs(Gref.to_scipy()) @ np.abs(rv)))[b:e] + 1e-300
+    ok_apply = bool(np.all(np.abs(z - zref[b:e]) <= bound))
     x, rep = F.pcg(torch.from_numpy(bvec[b:e].copy()).cuda(), tol=1e-8, max_iters=5000)
     stats = F.stats()
-    results[name] = {"G_bitwise": bool(ok_G), "Gt_bitwise": bool(ok_T), "apply_rel_diff": dz,
-                     "iters_N": rep["iters"], "iters_1": rep1.iters, "true_rel_res": rep["true_rel_res"],
+    results[name] = {"G_bitwise_vs_oracle": bool(ok_G), "Gt_bitwise_vs_oracle": bool(ok_T),
+                     "apply_within_bound_vs_oracle": ok_apply,
+                     "iters_N": rep["iters"], "iters_oracle": pr.iters, "true_rel_res": rep["true_rel_res"],
                      "halo_rows": stats["halo_rows"], "ms_total": stats["ms_total"], "ms_halo": stats["ms_halo"]}
     F.close()
-    ctx.close()
-    capi.afsai_factor_destroy(F1)
-    capi.afsai_ctx_destroy(h1)
+# error agreement: row n-1 has a tiny diagonal (psi < 0 at step 1 on the last rank only)
+B = ai.poisson3d(12)
+val = B.val.copy()
+last = B.n - 1
+val[B.rowptr[last]:B.rowptr[last + 1]][B.col[B.rowptr[last]:B.rowptr[last + 1]] == last] = 0.01
+B = ai.CSR(B.n, B.rowptr, B.col, val)
+try:
+    oracle.setup(B, 20, 2)
+    oracle_code = 0
+except oracle.OracleError as ex:
+    oracle_code = ex.code
+bounds = [B.n * q // world for q in range(world + 1)]
+b, e = bounds[rank], bounds[rank + 1]
+try:
+    Factor(ctx, DeviceCSR.from_numpy(B, row_begin=b, n_rows=e - b), 20, 2, 0.0, 1000).close()
+    code = 0
+except capi.AfsaiError as ex:
+    code = ex.code
+results["error_agreement"] = {"code": code, "oracle_code": oracle_code,
+                              "ok": code != 0 and (rank != world - 1 or code == capi.AFSAI_ENOTSPD)}
+ctx.close()
 allr = [None] * world
 dist.all_gather_object(allr, results)
 if rank == 0:
-    ok = all(r[c]["G_bitwise"] and r[c]["Gt_bitwise"] and abs(r[c]["iters_N"] - r[c]["iters_1"]) <= 1
-             and r[c]["apply_rel_diff"] < 1e-12 and r[c]["true_rel_res"] <= 1e-7 for r in allr for c in r)
+    ok = all(r[c]["G_bitwise_vs_oracle"] and r[c]["Gt_bitwise_vs_oracle"] and r[c]["apply_within_bound_vs_oracle"]
+             and abs(r[c]["iters_N"] - r[c]["iters_oracle"]) <= 1 and r[c]["true_rel_res"] <= 1e-7
+             for r in allr for c in r if c != "error_agreement")
+    ok = ok and all(r["error_agreement"]["ok"] for r in allr) and allr[0]["error_agreement"]["oracle_code"] == 2
     print(json.dumps({"world": world, "ok": ok, "ranks": allr}, indent=1))
 dist.destroy_process_group()

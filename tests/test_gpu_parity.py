@@ -79,6 +79,8 @@ CASES = [
     ("fe_4_10x2_cap15", lambda: ai.fe_elasticity(4), 10, 2, 0.0, 15),
     ("rsparse_s4", lambda: ai.random_sparse_spd(3000, 10, sub=6), 8, 4, 0.0, 1 << 30),
     ("hetero_32_probe", lambda: ai.hetero_poisson3d(32), 20, 2, 0.0, 1 << 30),
+    # hub column: G^T row 0 is ~n long (the long-row transpose sort, > 1024 entries)
+    ("arrow_3000_12x3", lambda: ai.arrow_spd(3000), 12, 3, 0.0, 1 << 30),
 ]
 
 
@@ -105,6 +107,8 @@ def test_setup_parity(ctx, name, make, k, s, eps, cap):
     Tr = oracle.transpose(Gr)
     assert np.array_equal(T.rowptr, Tr.rowptr) and np.array_equal(T.col, Tr.col)
     assert np.array_equal(T.val.view(np.int64), Tr.val.view(np.int64))
+    if name.startswith("arrow"):
+        assert np.diff(T.rowptr).max() > 2048, "the long-row transpose path was not exercised"
     F.close()
 
 
@@ -241,7 +245,7 @@ def test_determinism_repeat(ctx):
 @pytest.mark.parametrize("env", [{}, {"AFSAI_PROW": "0", "AFSAI_HITS": "0"}], ids=["default", "scan_kernel"])
 def test_block_setup_partition_emulation(ctx, make, k, s, cap, env, monkeypatch):
     """Rows of a block computed from a halo-extended copy of A (rows [b - k*beta, e)
-    only) are bitwise the same rows of the whole-matrix set-up (pin P12 on the GPU:
+    only) are bitwise the oracle's rows of the whole matrix (pin P12 on the GPU:
     the multi-GPU set-up's building block).  Also with the general
     scan kernel, whose last-step universe reaches one hop past the halo."""
     from paper_2010_14175_b200 import capi
@@ -249,8 +253,7 @@ def test_block_setup_partition_emulation(ctx, make, k, s, cap, env, monkeypatch)
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
     A = make()
-    F = gpu_setup(ctx, A, k, s, 0.0, cap)
-    G = host_csr(F)
+    G = oracle.setup(A, k, s, 0.0, cap, trace=False).to_csr(A.n)   # the reference is the oracle
     beta = A.bandwidth()
     n = A.n
     for b, e in [(0, n // 3), (n // 3, 2 * n // 3), (2 * n // 3, n)]:
@@ -262,9 +265,13 @@ def test_block_setup_partition_emulation(ctx, make, k, s, cap, env, monkeypatch)
         ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
         v = torch.empty(nnz, dtype=torch.float64, device="cuda")
         capi.afsai_factor_copy(h, 0, rp, ci, v)
+        # a block factor has no G^T: apply must refuse it (no illegal-address fault)
+        rr = torch.zeros(e - b, dtype=torch.float64, device="cuda")
+        with pytest.raises(capi.AfsaiError) as ex:
+            capi.afsai_apply(ctx.h, h, rr, torch.empty_like(rr))
+        assert ex.value.code == capi.AFSAI_EINVAL
         capi.afsai_factor_destroy(h)
         a0, a1 = G.rowptr[b], G.rowptr[e]
         assert np.array_equal(rp.cpu().numpy(), G.rowptr[b:e + 1] - a0)
         assert np.array_equal(ci.cpu().numpy(), G.col[a0:a1])
         assert np.array_equal(v.cpu().numpy().view(np.int64), G.val[a0:a1].view(np.int64))
-    F.close()
