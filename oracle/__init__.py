@@ -26,6 +26,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "afsai_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB32 = os.path.join(_HERE, "liboracle_f32.so")   # the same source with -DOR_FP32
 
 OK, EINVAL, ENOTSPD, ENOMEM, ENOTCONV = 0, 1, 2, 3, 6
 STOP_NAMES = {0: "kmax", 1: "cap", 2: "no_candidates", 3: "tolerance"}
@@ -38,15 +39,32 @@ class OracleError(RuntimeError):
 
 
 def build(force: bool = False) -> str:
-    """Compile liboracle.so (plain gcc, -ffp-contract=off, libm fma)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-pthread", "-o", _LIB, _SRC, "-lm"]
-        subprocess.check_call(cmd)
+    """Compile liboracle.so and liboracle_f32.so (plain gcc, -ffp-contract=off, libm fma)."""
+    for lib, extra in ((_LIB, []), (_LIB32, ["-DOR_FP32"])):
+        if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+            cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                   "-pthread"] + extra + ["-o", lib, _SRC, "-lm"]
+            subprocess.check_call(cmd)
     return _LIB
 
 
 _lib = None
+_lib32 = None
+
+
+def _load32():
+    """The single-precision set-up oracle (A_s = single(A), float arithmetic, G = double(G_s))."""
+    global _lib32
+    if _lib32 is None:
+        build()
+        lib = ctypes.CDLL(_LIB32)
+        P = ctypes.c_void_p
+        i64, i32, f64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+        lib.oracle_setup_rows.argtypes = [i64, P, P, P, i32, i32, f64, i32, P, i64, i32,
+                                          P, P, P, P, P, P, P, P, P, i32]
+        lib.oracle_setup_rows.restype = ctypes.c_int
+        _lib32 = lib
+    return _lib32
 
 
 def _load():
@@ -112,10 +130,18 @@ def mmax_of(n, nsteps, s, max_row_nnz):
 
 
 def setup(A, nsteps: int, s: int, eps: float = 0.0, max_row_nnz: int = 1 << 30,
-          rows=None, threads: int | None = None, trace: bool = True) -> SetupResult:
-    """aFSAI set-up of rows `rows` (default: all) of the full symmetric CSR A."""
-    lib = _load()
+          rows=None, threads: int | None = None, trace: bool = True, precision: str = "fp64") -> SetupResult:
+    """aFSAI set-up of rows `rows` (default: all) of the full symmetric CSR A.
+    precision="fp32": the single-precision set-up of P:953-965 -- A's values rounded
+    to float (A_s = single(A)), the whole set-up in float, G = double(G_s)."""
     rp, ci, v = _csr_arrays(A)
+    if precision == "fp32":
+        lib = _load32()
+        v = v.astype(np.float32)   # A_s = single(A), round to nearest even
+    elif precision == "fp64":
+        lib = _load()
+    else:
+        raise ValueError(precision)
     n = A.n
     rows = np.arange(n, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
     nr = len(rows)
@@ -210,8 +236,8 @@ def pcg(A, G, Gt, b: np.ndarray, tol: float = 1e-8, max_iters: int = 10000) -> P
     return PcgResult(x, int(it[0]), float(rel[0]), rc == OK, hist[: int(it[0]) + 1])
 
 
-def setup_full(A, nsteps, s, eps=0.0, max_row_nnz=1 << 30, threads=None):
+def setup_full(A, nsteps, s, eps=0.0, max_row_nnz=1 << 30, threads=None, precision="fp64"):
     """Convenience: (G, Gt, SetupResult) for all rows."""
-    res = setup(A, nsteps, s, eps, max_row_nnz, threads=threads)
+    res = setup(A, nsteps, s, eps, max_row_nnz, threads=threads, precision=precision)
     G = res.to_csr(A.n)
     return G, transpose(G), res

