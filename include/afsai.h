@@ -82,7 +82,12 @@ typedef struct {
     int32_t s;             /* 1 <= s <= AFSAI_MAX_S: entries added per step          */
     double eps;            /* 0 <= eps < 1: stop a row when psi_k/psi_0 <= eps (Eq.16)*/
     int32_t max_row_nnz;   /* >= 1: cap on nnz of a row of G, diagonal included (R8)  */
+    int32_t precision;     /* set-up arithmetic: AFSAI_PREC_FP64 (0, default) or
+                              AFSAI_PREC_FP32 (§4.3: A_s = single(A),
+                              the set-up in fp32, G = double(G_s); apply/PCG stay fp64) */
 } afsai_params_t;
+#define AFSAI_PREC_FP64 0
+#define AFSAI_PREC_FP32 1
 
 typedef struct {
     int32_t code;          /* AFSAI_* */

@@ -94,10 +94,12 @@ class Factor:
     """G (and G^T) of one afsai_setup call."""
 
     def __init__(self, ctx: Context, A: DeviceCSR, nsteps: int, s: int, eps: float = 0.0,
-                 max_row_nnz: int = 1 << 30):
+                 max_row_nnz: int = 1 << 30, precision: str = "fp64"):
+        """precision="fp32": the single-precision set-up; G is fp64 either way."""
         self.ctx = ctx
         self.A = A
-        self.h = capi.afsai_setup(ctx.h, A.c(), nsteps, s, eps, min(max_row_nnz, 2**31 - 1))
+        self.h = capi.afsai_setup(ctx.h, A.c(), nsteps, s, eps, min(max_row_nnz, 2**31 - 1),
+                                  capi.PRECISIONS[precision])
 
     @property
     def nnz(self):

@@ -49,10 +49,14 @@ def _flags_for(src: str):
     # -fmad=false, so the only fused multiply-adds are the explicit fma() of the
     # arithmetic contract.  The decision is made from the file's
     # includes, not its name; setup_common.cuh #errors without AFSAI_FMAD_OFF.
-    with open(src) as f:
-        if _CONTRACT_HDR.search(f.read()):
-            flags += ["-fmad=false", "-DAFSAI_FMAD_OFF"]
+    if _is_contract(src):
+        flags += ["-fmad=false", "-DAFSAI_FMAD_OFF"]
     return flags
+
+
+def _is_contract(src: str) -> bool:
+    with open(src) as f:
+        return bool(_CONTRACT_HDR.search(f.read()))
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False, variant: str = "",
@@ -75,16 +79,20 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, varia
     newest_hdr = max(os.path.getmtime(h) for h in hdrs)
     objs, todo = [], []
     for s in srcs:
-        o = os.path.join(objdir, os.path.basename(s) + ".o")
-        objs.append(o)
-        if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
-            todo.append((s, o))
+        # set-up units twice: fp64 (afsai::dp) and fp32 (afsai::sp, -DAFSAI_SETUP_FP32)
+        variants = [("", [])] + ([(".f32", ["-DAFSAI_SETUP_FP32"])] if _is_contract(s) else [])
+        for suffix, vflags in variants:
+            o = os.path.join(objdir, os.path.basename(s) + suffix + ".o")
+            objs.append(o)
+            if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), newest_hdr):
+                todo.append((s, o, vflags))
 
     def compile_one(so):
-        s, o = so
-        cmd = [NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s) + extra
+        s, o, vflags = so
+        cmd = ([NVCC, "-c", s, "-o", o, "-I", inc, "-I", os.path.join(ROOT, "include")] + _flags_for(s) + extra +
+               vflags)
         r = subprocess.run(cmd, capture_output=True, text=True)
-        with open(os.path.join(objdir, os.path.basename(s) + ".ptxas.txt"), "w") as f:
+        with open(o[:-2] + ".ptxas.txt", "w") as f:
             f.write(r.stderr)
         return s, r
 

@@ -39,7 +39,7 @@ class afsai_csr_t(ctypes.Structure):
 
 class afsai_params_t(ctypes.Structure):
     _fields_ = [("nsteps", ctypes.c_int32), ("s", ctypes.c_int32), ("eps", ctypes.c_double),
-                ("max_row_nnz", ctypes.c_int32)]
+                ("max_row_nnz", ctypes.c_int32), ("precision", ctypes.c_int32)]
 
 
 class afsai_status_t(ctypes.Structure):
@@ -188,8 +188,12 @@ def afsai_ctx_launches(ctx) -> int:
     return int(lib().afsai_ctx_launches(ctx))
 
 
-def afsai_setup(ctx, A: afsai_csr_t, nsteps: int, s: int, eps: float, max_row_nnz: int):
-    p = afsai_params_t(nsteps, s, eps, max_row_nnz)
+AFSAI_PREC_FP64, AFSAI_PREC_FP32 = 0, 1
+PRECISIONS = {"fp64": AFSAI_PREC_FP64, "fp32": AFSAI_PREC_FP32}
+
+
+def afsai_setup(ctx, A: afsai_csr_t, nsteps: int, s: int, eps: float, max_row_nnz: int, precision: int = 0):
+    p = afsai_params_t(nsteps, s, eps, max_row_nnz, precision)
     f = ctypes.c_void_p()
     st = afsai_status_t()
     rc = lib().afsai_setup(ctx, ctypes.byref(A), ctypes.byref(p), ctypes.byref(f), ctypes.byref(st))
@@ -282,8 +286,8 @@ def afsai_ctx_kernel_times(ctx) -> dict:
 
 
 def afsai_setup_block(ctx, A_ext: afsai_csr_t, row_lo: int, n_rows: int, nsteps: int, s: int, eps: float,
-                      max_row_nnz: int):
-    p = afsai_params_t(nsteps, s, eps, max_row_nnz)
+                      max_row_nnz: int, precision: int = 0):
+    p = afsai_params_t(nsteps, s, eps, max_row_nnz, precision)
     f = ctypes.c_void_p()
     st = afsai_status_t()
     rc = lib().afsai_setup_block(ctx, ctypes.byref(A_ext), int(row_lo), int(n_rows), ctypes.byref(p),

@@ -84,6 +84,27 @@ __global__ void symmetry_kernel(const int64_t *rowptr, const int32_t *col, const
     }
 }
 
+// A_s = single(A) for the fp32 set-up (the paper casts on the
+// host before the copy; here A is already on the device).  Round to nearest even
+// (__double2float_rn, numpy's astype(float32)).  Flags (lowest row) a value that
+// overflows to +-inf or a diagonal that is no longer > 0.
+__global__ void cast_rows_f32_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                     int64_t n_rows, int64_t row_begin, float *out, unsigned long long *err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw) {
+        const int64_t e0 = rowptr[r] - base, e1 = rowptr[r + 1] - base;
+        bool bad = false;
+        for (int64_t e = e0 + lane; e < e1; e += 32) {
+            const float f = __double2float_rn(val[e]);
+            out[e] = f;
+            bad |= isinf(f) || (col[e] == r + row_begin && !(f > 0.0f));
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicMin(err, (unsigned long long)(r + row_begin));
+    }
+}
+
 // ---------------------------------------------------------------- exclusive scan
 // int32 counts -> int64 offsets, out[n] = total.  Three passes over tiles of
 // kScanTile elements: tile sums, scan of tile sums (one block), tile scans.

@@ -7,6 +7,8 @@
 namespace afsai {
 __global__ void validate_rows_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
                                      int64_t n_rows, int64_t row_begin, int64_t n_cols, unsigned long long *err);
+__global__ void cast_rows_f32_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                     int64_t n_rows, int64_t row_begin, float *out, unsigned long long *err);
 __global__ void row_len_max_kernel(const int64_t *rowptr, int64_t n_rows, unsigned long long *out);
 __global__ void symmetry_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
                                 int64_t n_rows, int64_t row_begin, unsigned long long *err);

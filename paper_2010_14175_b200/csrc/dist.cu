@@ -834,7 +834,8 @@ int afsai_setup_block(afsai_ctx_t ctx, const afsai_csr_t *Ain, int64_t row_lo, i
     if (Ain->n_rows < 1 || Ain->n_cols < 1 || a_hi > Ain->n_cols || n_rows < 0 || row_lo < a_lo ||
         row_lo + n_rows > a_hi || !Ain->rowptr || !Ain->col || !Ain->val)
         return set_status(status, AFSAI_EINVAL, "block must lie inside A_ext");
-    if (p->nsteps < 0 || p->s < 1 || p->s > AFSAI_MAX_S || !(p->eps >= 0.0 && p->eps < 1.0) || p->max_row_nnz < 1)
+    if (p->nsteps < 0 || p->s < 1 || p->s > AFSAI_MAX_S || !(p->eps >= 0.0 && p->eps < 1.0) || p->max_row_nnz < 1 ||
+        (p->precision != AFSAI_PREC_FP64 && p->precision != AFSAI_PREC_FP32))
         return set_status(status, AFSAI_EINVAL, "params out of range");
     if (std::min<int64_t>((int64_t)p->nsteps * p->s, (int64_t)p->max_row_nnz - 1) > AFSAI_MAX_MMAX)
         return set_status(status, AFSAI_ELIMIT, "min(nsteps*s, max_row_nnz-1) exceeds AFSAI_MAX_MMAX (128)");

@@ -152,6 +152,38 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     // The candidate table starts small (stencil universes are small); rows that
     // overflow an on-chip table are retried with 4x larger tables.
     // AFSAI_LPR / AFSAI_TABLE / AFSAI_HITS=0 override (experiments).
+    // the kernel instances of the set-up precision (afsai::dp fp64, afsai::sp fp32)
+    const bool f32 = p.precision == AFSAI_PREC_FP32;
+    auto scan_kernel_for = f32 ? sp::scan_kernel_for : dp::scan_kernel_for;
+    auto scan_row_bytes = f32 ? sp::scan_row_bytes : dp::scan_row_bytes;
+    auto hits_kernel_for = f32 ? sp::hits_kernel_for : dp::hits_kernel_for;
+    auto hits_row_bytes = f32 ? sp::hits_row_bytes : dp::hits_row_bytes;
+    auto lockstep_kernel_for = f32 ? sp::lockstep_kernel_for : dp::lockstep_kernel_for;
+    auto prow_kernel_for = f32 ? sp::prow_kernel_for : dp::prow_kernel_for;
+    auto prow_row_bytes = f32 ? sp::prow_row_bytes : dp::prow_row_bytes;
+    DevBuf val32;  // A_s = single(A) (fp32 set-up)
+    if (f32) {
+        AFSAI_CUDA_TRY(val32.alloc(std::max<int64_t>(Aext.nnz, 1) * sizeof(float), ctx->stream));
+        DevBuf cerr;
+        AFSAI_CUDA_TRY(cerr.alloc(sizeof(unsigned long long), ctx->stream));
+        AFSAI_CUDA_TRY(cudaMemsetAsync(cerr.p, 0xff, sizeof(unsigned long long), ctx->stream));
+        const int grid = std::max<int64_t>(1, std::min<int64_t>((Aext.n_rows * 32 + 255) / 256, grid_stream(ctx)));
+        {
+            KTimer kt(ctx, AFSAI_K_ASSEMBLE);
+            cast_rows_f32_kernel<<<grid, 256, 0, ctx->stream>>>(Aext.rowptr, Aext.col, Aext.val, Aext.base,
+                                                                 Aext.n_rows, Aext.row_begin, val32.as<float>(),
+                                                                 cerr.as<unsigned long long>());
+        }
+        ctx->launches += 1;
+        AFSAI_CUDA_TRY(cudaGetLastError());
+        unsigned long long ce = 0;
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(&ce, cerr.p, sizeof ce, cudaMemcpyDeviceToHost, ctx->stream));
+        AFSAI_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (ce != ~0ull)
+            return set_status(status, AFSAI_EINVAL,
+                              "A_s = single(A) overflows fp32 or loses a positive diagonal (fp32 set-up)",
+                              (int64_t)ce);
+    }
     int lpr = mmax <= 96 ? 16 : 32;
     if (const char *e = std::getenv("AFSAI_LPR")) {
         const int l = std::atoi(e);
@@ -197,6 +229,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     a.rowptr = Aext.rowptr;
     a.col = Aext.col;
     a.val = Aext.val;
+    a.val32 = f32 ? val32.as<float>() : nullptr;
     a.base = Aext.base;
     a.nnz = Aext.nnz;
     a.a_lo = a_lo;
@@ -282,7 +315,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             stats->plan = (hits && lockstep) ? AFSAI_PLAN_LOCKSTEP : prow ? AFSAI_PLAN_PROW
                                                              : hits ? AFSAI_PLAN_HITS : AFSAI_PLAN_SCAN;
             stats->lanes_per_row = lpr;
-            stats->value_bytes = 8;
+            stats->value_bytes = f32 ? 4 : 8;
         }
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.work.p, 0, sizeof(unsigned long long), ctx->stream));
         AFSAI_CUDA_TRY(cudaMemsetAsync(W.retry_count.p, 0, sizeof(int32_t), ctx->stream));
@@ -620,8 +653,10 @@ int afsai_setup(afsai_ctx_t ctx, const afsai_csr_t *A, const afsai_params_t *p, 
     if (A->n_rows < 0 || A->n_cols < 1 || A->nnz < 0 || A->row_begin < 0 || A->row_begin + A->n_rows > A->n_cols ||
         A->n_cols >= (int64_t)INT32_MAX || (A->n_rows > 0 && (!A->rowptr || !A->col || !A->val)))
         return set_status(status, AFSAI_EINVAL, "bad matrix sizes or null arrays");
-    if (p->nsteps < 0 || p->s < 1 || p->s > AFSAI_MAX_S || !(p->eps >= 0.0 && p->eps < 1.0) || p->max_row_nnz < 1)
-        return set_status(status, AFSAI_EINVAL, "params out of range (nsteps>=0, 1<=s<=16, 0<=eps<1, max_row_nnz>=1)");
+    if (p->nsteps < 0 || p->s < 1 || p->s > AFSAI_MAX_S || !(p->eps >= 0.0 && p->eps < 1.0) || p->max_row_nnz < 1 ||
+        (p->precision != AFSAI_PREC_FP64 && p->precision != AFSAI_PREC_FP32))
+        return set_status(status, AFSAI_EINVAL,
+                          "params out of range (nsteps>=0, 1<=s<=16, 0<=eps<1, max_row_nnz>=1, precision 0|1)");
     const int64_t mmax64 = std::min<int64_t>((int64_t)p->nsteps * p->s, (int64_t)p->max_row_nnz - 1);
     if (mmax64 > AFSAI_MAX_MMAX)
         return set_status(status, AFSAI_ELIMIT, "min(nsteps*s, max_row_nnz-1) exceeds AFSAI_MAX_MMAX (128)");

@@ -13,7 +13,39 @@
 #include "afsai_internal.h"
 #include "setup_kernel.h"
 
+// Precision of the set-up arithmetic.  Every set-up translation unit is compiled
+// twice (build.py): as afsai::dp (fp64, `real` = double; the default set-up) and,
+// with -DAFSAI_SETUP_FP32, as afsai::sp (`real` = float: the single-precision
+// set-up of PAPER.md §4.3, on A_s = single(A)).  The contract C1-C12
+// is the same in both; the fp32 oracle (oracle/ built with -DOR_FP32) pins sp.
+// Comparisons against the double constants 1e-30 and eps widen the float operand
+// exactly (as the oracle does); the output scratch is fp64: G = double(G_s).
+#ifdef AFSAI_SETUP_FP32
+#define AFSAI_PNS sp
+#else
+#define AFSAI_PNS dp
+#endif
+
 namespace afsai {
+namespace AFSAI_PNS {
+
+#ifdef AFSAI_SETUP_FP32
+typedef float real;
+#else
+typedef double real;
+#endif
+
+// A's values in the set-up's precision (A_s for the fp32 set-up)
+__device__ __forceinline__ const real *aval(const SetupKArgs &a) {
+#ifdef AFSAI_SETUP_FP32
+    return a.val32;
+#else
+    return a.val;
+#endif
+}
+
+// bytes of n values, padded so what follows stays 16-byte aligned
+__host__ __device__ inline int64_t real_bytes(int64_t n) { return (n * (int64_t)sizeof(real) + 15) & ~int64_t(15); }
 
 constexpr int32_t kEmpty = -1;
 constexpr int8_t kCand = -2;
@@ -82,7 +114,7 @@ __device__ __forceinline__ int hinsert(int32_t *hkey, int H, int log2H, int32_t 
 __device__ __forceinline__ int tri(int q) { return (q * (q + 1)) >> 1; }
 
 // (|a|, ja) better than (|b|, jb)?  |acc| descending, then column ascending.
-__device__ __forceinline__ bool better(double aa, int32_t ja, double ab, int32_t jb) {
+__device__ __forceinline__ bool better(real aa, int32_t ja, real ab, int32_t jb) {
     return (aa > ab) || (aa == ab && ja < jb);
 }
 
@@ -120,30 +152,30 @@ __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {
 // instruction-cache sensitive).  Every accumulator folds in k-ascending order,
 // exactly DESIGN.md C5.  Returns false on a pivot !(> 1e-30).
 template <int LPR, int NT, int GS, class State>
-__device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs, int ug, double &psi) {
+__device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs, int ug, real &psi) {
     const int M = w.M, gl = G.gl;
-    double t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
-    double *Lnew[GS];
-    const double *Lr[NT];
+    real t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
+    real *Lnew[GS];
+    const real *Lr[NT];
 #pragma unroll
     for (int u = 0; u < GS; ++u) {
-        const double *ar = w.arow + (ug + u) * M;
+        const real *ar = w.arow + (ug + u) * M;
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt) {
             const int c = gl + LPR * tt;
-            t[u][tt] = (u < gs && c < qf) ? ar[c] : 0.0;
+            t[u][tt] = (u < gs && c < qf) ? ar[c] : real(0);
         }
-        dg[u] = (u < gs) ? ar[qf + u] : 0.0;
+        dg[u] = (u < gs) ? ar[qf + u] : real(0);
 #pragma unroll
-        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && u < gs) ? ar[qf + v] : 0.0;
-        ty[u] = (u < gs) ? -w.brow[ug + u] : 0.0;
+        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && u < gs) ? ar[qf + v] : real(0);
+        ty[u] = (u < gs) ? -w.brow[ug + u] : real(0);
         Lnew[u] = w.L + tri(qf + u < M ? qf + u : 0);
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
         Lr[tt] = (c < qf) ? w.L + tri(c) : w.L;  // dead columns: any in-bounds row
-        ivc[tt] = (c < qf) ? w.inv[c] : 0.0;
+        ivc[tt] = (c < qf) ? w.inv[c] : real(0);
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
@@ -152,11 +184,11 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 #pragma unroll 1
         for (int ln = 0; ln < lnend; ++ln) {
             const int k = LPR * tt + ln;
-            const double y_k = w.y[k];
-            double lsm[NT];
+            const real y_k = w.y[k];
+            real lsm[NT];
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
-            double l[GS];
+            real l[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
             // broadcast values: every lane stores the same bits (no divergent branch
@@ -184,18 +216,18 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
     for (int uf = 0; uf < GS; ++uf) {
         if (uf >= gs) break;
         const int k = qf + uf;
-        const double piv = dg[uf];
+        const real piv = dg[uf];
         if (!(piv > 1e-30)) return false;
-        const double dq = sqrt(piv);  // C5.2: two correctly rounded operations
-        const double inv_k = 1.0 / dq;
-        const double y_k = ty[uf] * inv_k;
+        const real dq = sqrt(piv);  // C5.2: two correctly rounded operations
+        const real inv_k = real(1) / dq;
+        const real y_k = ty[uf] * inv_k;
         psi = fma(-y_k, y_k, psi);     // C6
         w.inv[k] = inv_k;  // redundant values: every lane stores the same bits
         w.y[k] = y_k;
-        double lu[GS];
+        real lu[GS];
 #pragma unroll
         for (int u = 0; u < GS; ++u) {
-            lu[u] = 0.0;
+            lu[u] = real(0);
             if (u > uf && u < gs) {
                 lu[u] = cp[u][uf] * inv_k;
                 Lnew[u][k] = lu[u];
@@ -226,14 +258,14 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 template <int LPR, int NT, class State>
 __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
     const int gl = G.gl;
-    double tb[NT], ivc[NT];
+    real tb[NT], ivc[NT];
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
-        tb[tt] = (c < m) ? w.y[c] : 0.0;
-        ivc[tt] = (c < m) ? w.inv[c] : 0.0;
+        tb[tt] = (c < m) ? w.y[c] : real(0);
+        ivc[tt] = (c < m) ? w.inv[c] : real(0);
     }
-    const double *pk = w.L + tri(m > 0 ? m - 1 : 0) + gl;
+    const real *pk = w.L + tri(m > 0 ? m - 1 : 0) + gl;
 #pragma unroll
     for (int tt = NT - 1; tt >= 0; --tt) {
         int ln0 = m - 1 - LPR * tt;
@@ -241,11 +273,11 @@ __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
 #pragma unroll 1
         for (int ln = ln0; ln >= 0; --ln) {
             const int k = LPR * tt + ln;
-            double lk[NT];
+            real lk[NT];
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];
             pk -= k;
-            const double gk = G.bcast(tb[tt] * ivc[tt], ln);
+            const real gk = G.bcast(tb[tt] * ivc[tt], ln);
             w.g[k] = gk;  // broadcast value, stored by every lane
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
@@ -254,4 +286,5 @@ __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
     G.sync();
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -2,6 +2,7 @@
 #include "setup_hits.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 // ======================================================================
 // Hit-list variant for matrices with short rows (max row length - 1 <= HC).
@@ -21,7 +22,7 @@ namespace afsai {
 // through a group-aggregated allocation (free stack first, then high-water).
 template <int LPR, int HC>
 __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int log2H, int32_t i, bool valid,
-                              int32_t c, double v, int q, double *arow_u, double *brow_u) {
+                              int32_t c, real v, int q, real *arow_u, real *brow_u) {
     const int CA = w.CA;
     const int32_t r = q < 0 ? i : w.P[q];
     bool need = false;
@@ -116,19 +117,19 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             w.misc[1] = 0;
             w.misc[2] = 0;
             w.misc[3] = 0;
-            w.dscr[0] = 0.0;
+            w.dscr[0] = real(0);
         }
         G.sync();
         // universe = columns j < i of row i, each with its hit (i, a_ji)
         {
             const bool vi = gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
-            const double xi = vi ? __ldg(a.val + e0i + gl) : 0.0;
+            const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
             scan_row_hits<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr);
         }
-        const double a_ii = w.dscr[0];
-        const double psi0 = a_ii;
-        double psi = psi0;
+        const real a_ii = w.dscr[0];
+        const real psi0 = a_ii;
+        real psi = psi0;
         int m = 0, steps = 0, reason = AFSAI_STOP_KMAX;
         bool fail = false, overflow = (w.misc[1] != 0);
         int fail_step = 0;
@@ -140,34 +141,34 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             // ---- phase G: gradient = fold of each active candidate's hits (C3)
             const int hw = w.misc[2];
             int nc = 0;
-            double ba[GS];
+            real ba[GS];
             int32_t bj[GS], bt[GS];
 #pragma unroll
-            for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = 0x7fffffff; bt[q] = -1; }
+            for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = 0x7fffffff; bt[q] = -1; }
             for (int aa = gl; aa < hw; aa += LPR) {
                 const int n = w.ahn[aa];
                 if (n == 0) continue;  // free slot
-                double acc = 0.0;
+                real acc = real(0);
 #pragma unroll
                 for (int h = 0; h < HC; ++h) {
                     if (h < n) {
                         const int q = w.ahq[h * CA + aa];
-                        const double gv = q < 0 ? 1.0 : w.g[q];
+                        const real gv = q < 0 ? real(1) : w.g[q];
                         acc = fma(w.hv[h * CA + aa], gv, acc);
                     }
                 }
                 c_gfma += n;
                 if (use_acc) w.acc[aa] = acc;
-                if (acc != 0.0) {
+                if (acc != real(0)) {
                     ++nc;
                     if (!use_acc) {
-                        double ca = fabs(acc);
+                        real ca = fabs(acc);
                         int32_t cj = w.akey[aa];
                         int32_t ct = aa;
 #pragma unroll
                         for (int q = 0; q < GS; ++q) {
                             if (better(ca, cj, ba[q], bj[q])) {
-                                const double ta = ba[q];
+                                const real ta = ba[q];
                                 const int32_t tj = bj[q], t2 = bt[q];
                                 ba[q] = ca; bj[q] = cj; bt[q] = ct;
                                 ca = ta; cj = tj; ct = t2;
@@ -183,11 +184,11 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             // ---- phase S: top-nsel under (|acc| desc, j asc)
             if (!use_acc) {
                 for (int u = 0; u < nsel; ++u) {
-                    double wa = ba[0];
+                    real wa = ba[0];
                     int32_t wj = bj[0];
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) {
-                        const double oa = G.xorv(wa, o);
+                        const real oa = G.xorv(wa, o);
                         const int32_t oj = G.xorv(wj, o);
                         if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
                     }
@@ -196,23 +197,23 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                         w.sela[u] = bt[0];
 #pragma unroll
                         for (int q = 0; q + 1 < GS; ++q) { ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1]; }
-                        ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                        ba[GS - 1] = -real(1); bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
                     }
                 }
             } else {
                 for (int u = 0; u < nsel; ++u) {
-                    double xa = -1.0;
+                    real xa = -real(1);
                     int32_t xj = 0x7fffffff, xt = -1;
                     for (int aa = gl; aa < hw; aa += LPR) {
                         if (w.ahn[aa] <= 0) continue;
-                        const double av = fabs(w.acc[aa]);
-                        if (av == 0.0) continue;
+                        const real av = fabs(w.acc[aa]);
+                        if (av == real(0)) continue;
                         const int32_t j = w.akey[aa];
                         if (better(av, j, xa, xj)) { xa = av; xj = j; xt = aa; }
                     }
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) {
-                        const double oa = G.xorv(xa, o);
+                        const real oa = G.xorv(xa, o);
                         const int32_t oj = G.xorv(xj, o);
                         const int32_t ot = G.xorv(xt, o);
                         if (better(oa, oj, xa, xj)) { xa = oa; xj = oj; xt = ot; }
@@ -240,8 +241,8 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                 w.ahn[aa] = 0;
                 w.afree[w.misc[3] + gl] = (int16_t)aa;
             }
-            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = 0.0;
-            if (gl < nsel) w.brow[gl] = 0.0;
+            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = real(0);
+            if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             if (gl == 0) w.misc[3] += nsel;
             G.sync();
@@ -249,13 +250,13 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             // ---- phase A: gather the new rows (one row per pass), record hits
             for (int ug = 0; ug < nsel; ug += GS) {
                 int32_t pc[GS];
-                double pv[GS];
+                real pv[GS];
                 bool pvld[GS];
 #pragma unroll
                 for (int u = 0; u < GS; ++u) {  // every row's entries in flight at once
                     pvld[u] = (ug + u < nsel) && gl < w.glen[ug + u];
                     pc[u] = pvld[u] ? __ldg(a.col + w.gstart[ug + u] + gl) : 0;
-                    pv[u] = pvld[u] ? __ldg(a.val + w.gstart[ug + u] + gl) : 0.0;
+                    pv[u] = pvld[u] ? __ldg(aval(a) + w.gstart[ug + u] + gl) : real(0);
                 }
 #pragma unroll
                 for (int u = 0; u < GS; ++u)
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                 c_border += (unsigned long long)(q * (q - 1) / 2 + 2 * q + 1);
             }
             m += nsel;
-            if (!(psi > 0.0)) { fail = true; fail_step = k; break; }
+            if (!(psi > real(0))) { fail = true; fail_step = k; break; }
             PHASE(4)
             back_substitute<LPR, NT>(w, G, m);
             c_back += (unsigned long long)(m * (m - 1) / 2);
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             G.sync();
             continue;
         }
-        const double d = 1.0 / sqrt(psi);
+        const real d = real(1) / sqrt(psi);
         int32_t *oc = a.scol + orow * a.stride;
         double *ov = a.sval + orow * a.stride;
 #pragma unroll
@@ -353,9 +354,11 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
     }
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai
 
 namespace afsai {
+namespace AFSAI_PNS {
 // ---------------------------------------------------------------- host side
 template <int LPR, int NT, int HC>
 static SetupKernFn hits_gs(int gs) {
@@ -392,4 +395,5 @@ int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc) {
     const int gs = s < kMaxGroup ? s : kMaxGroup;
     return hc <= 6 ? hit_state_bytes<6>(H, mmax, s, cact, s > gs) : hit_state_bytes<8>(H, mmax, s, cact, s > gs);
 }
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -4,9 +4,10 @@
 #include "setup_common.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 struct HitState {
-    double *inv, *y, *g, *L, *arow, *brow, *dscr, *hv, *acc;
+    real *inv, *y, *g, *L, *arow, *brow, *dscr, *hv, *acc;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey;
     int16_t *ahs, *afree;
@@ -22,7 +23,7 @@ __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, 
     int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA;
     int64_t i16 = 2 * (int64_t)CA;
     int64_t i8 = (int64_t)H + CA + (int64_t)CA * HC;
-    int64_t b = dbl * 8 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
+    int64_t b = real_bytes(dbl) + i64 * 8 + i32 * 4 + i16 * 2 + i8;
     return (b + 15) & ~int64_t(15);
 }
 
@@ -32,7 +33,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     const int H = a.H, M = a.mmax, S = a.s, CA = a.cact;
     w.M = M;
     w.CA = CA;
-    double *d = reinterpret_cast<double *>(base);
+    real *d = reinterpret_cast<real *>(base);
     // g first: the lockstep fast paths prefetch inv[-1] / y[-1] (unused values) and
     // read up to 31 doubles past the end of L (into arow), all inside the row's region
     w.g = d; d += M;
@@ -45,7 +46,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.hv = d; d += CA * HC;  // [h][a]
     w.acc = nullptr;
     if (acc) { w.acc = d; d += CA; }
-    int64_t *l8 = reinterpret_cast<int64_t *>(d);
+    int64_t *l8 = reinterpret_cast<int64_t *>(base + real_bytes(d - reinterpret_cast<real *>(base)));
     w.gstart = l8; l8 += S;
     int32_t *ip = reinterpret_cast<int32_t *>(l8);
     w.hkey = ip; ip += H;
@@ -70,7 +71,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
 // Insert the hit (column r at pattern position q, value v) into active slot aa,
 // keeping the list sorted by r; q = -1 stands for r = i (always last).
 template <int HC>
-__device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int32_t r, double v) {
+__device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int32_t r, real v) {
     const int CA = w.CA;
     int n = w.ahn[aa];
     if (n >= HC) {
@@ -91,4 +92,5 @@ __device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int
     w.ahn[aa] = (int8_t)(n + 1);
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -10,7 +10,8 @@ struct SetupKArgs {
     // A: global rows [a_lo, a_hi); entries of row r: [rowptr[r-a_lo]-base, rowptr[r-a_lo+1]-base)
     const int64_t *rowptr;
     const int32_t *col;
-    const double *val;
+    const double *val;    // fp64 set-up (afsai::dp kernels)
+    const float *val32;   // fp32 set-up (afsai::sp kernels): A_s = single(A), same layout
     int64_t base, a_lo, a_hi;
     int64_t nnz;  // entries of A_ext (bounds checks of the debug build)
     // rows to compute: rows ? rows[t] : row_lo + t, for t < nrows
@@ -40,16 +41,28 @@ struct SetupKArgs {
 
 using SetupKernFn = void (*)(SetupKArgs);
 
-// general kernel: candidates' rows of A re-read every step (any row length)
-SetupKernFn scan_kernel_for(int lpr, int mmax, int s);
-int64_t scan_row_bytes(int H, int mmax, int s);
-// hit-list kernel: rows of A with at most hc + 1 entries (stencils)
-SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);
-int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);
-// hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4, mmax <= 6*lpr)
-SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);
-// pattern-row kernel (long rows, s <= 4, mmax <= 128, rows <= 128 entries): 32 lanes per row
-SetupKernFn prow_kernel_for(int mmax, int s, int64_t max_row_len);
-int64_t prow_row_bytes(int H, int mmax, int s, int lcap);
+// The kernel factories exist twice: afsai::dp (fp64 set-up) and afsai::sp (fp32
+// set-up); the same sources compiled with and without
+// -DAFSAI_SETUP_FP32 (setup_common.cuh).
+#define AFSAI_SETUP_FACTORIES                                                                        \
+    /* general kernel: candidates' rows of A re-read every step (any row length) */                  \
+    SetupKernFn scan_kernel_for(int lpr, int mmax, int s);                                             \
+    int64_t scan_row_bytes(int H, int mmax, int s);                                                    \
+    /* hit-list kernel: rows of A with at most hc + 1 entries (stencils) */                          \
+    SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);                                     \
+    int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);                                  \
+    /* hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4,                 \
+       mmax <= 6*lpr) */                                                                               \
+    SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);                                 \
+    /* pattern-row kernel (long rows, s <= 4, mmax <= 128, rows <= 128 entries): 32 lanes per row */   \
+    SetupKernFn prow_kernel_for(int mmax, int s, int64_t max_row_len);                                 \
+    int64_t prow_row_bytes(int H, int mmax, int s, int lcap);
+namespace dp {
+AFSAI_SETUP_FACTORIES
+}  // namespace dp
+namespace sp {
+AFSAI_SETUP_FACTORIES
+}  // namespace sp
+#undef AFSAI_SETUP_FACTORIES
 
 }  // namespace afsai

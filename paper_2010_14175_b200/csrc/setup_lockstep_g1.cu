@@ -3,6 +3,7 @@
 #include "setup_lockstep_impl.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 template SetupKernFn ls_instance<1>(int lpr, int nt, int hc);
 extern template SetupKernFn ls_instance<2>(int lpr, int nt, int hc);
 extern template SetupKernFn ls_instance<3>(int lpr, int nt, int hc);
@@ -22,4 +23,5 @@ SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc) {
         default: return ls_instance<4>(lpr, nt, hc);
     }
 }
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -2,5 +2,7 @@
 #include "setup_lockstep_impl.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 template SetupKernFn ls_instance<3>(int lpr, int nt, int hc);
+}  // namespace AFSAI_PNS
 }  // namespace afsai

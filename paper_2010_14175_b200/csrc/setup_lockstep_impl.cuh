@@ -15,6 +15,7 @@
 #include "setup_hits.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 constexpr unsigned kAll = 0xffffffffu;
 
@@ -58,7 +59,7 @@ struct RowBook {
 
 // hit_insert of setup_hits.cuh; returns false when the list is full
 template <int HC>
-__device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, int32_t r, double v) {
+__device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, int32_t r, real v) {
     const int CA = w.CA;
     const int n = w.ahn[aa];
     if (n >= HC) return false;
@@ -85,7 +86,7 @@ __device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, 
 // tables to the next call.
 template <int LPR, int HC>
 __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H, int log2H, int32_t i, bool valid,
-                                 int32_t c, double v, int q, double *arow_u, double *brow_u, RowBook &b) {
+                                 int32_t c, real v, int q, real *arow_u, real *brow_u, RowBook &b) {
     const int CA = w.CA;
     bool need = false;
     int sl = -1;
@@ -134,12 +135,17 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
     G.sync();
 }
 
-// predicated fp64 fma: if (p) d = fma(a, b, d), as one predicated DFMA (no selects,
+// predicated fma: if (p) d = fma(a, b, d), as one predicated DFMA / FFMA (no selects,
 // no temporaries; a plain `if` around fma() compiles to DFMA + two moves)
 __device__ __forceinline__ void fma_if(bool p, double a, double b, double &d) {
     asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
         : "+d"(d)
         : "d"(a), "d"(b), "r"((int)p));
+}
+__device__ __forceinline__ void fma_if(bool p, float a, float b, float &d) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q fma.rn.f32 %0, %1, %2, %0;\n\t}"
+        : "+f"(d)
+        : "f"(a), "f"(b), "r"((int)p));
 }
 
 // Bordered Cholesky of the new rows q = qf .. qf+gs-1 (arow slots ug..), forward
@@ -160,26 +166,26 @@ __device__ __forceinline__ void fma_if(bool p, double a, double b, double &d) {
 // when its code grows.  Returns false on a pivot !(> 1e-30).
 template <int LPR, int NT, int GS>
 __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool active, int qf, int gs, int ug,
-                                int qf_max, double &psi) {
+                                int qf_max, real &psi) {
     const int M = w.M, gl = G.gl;
-    double t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
-    double *Lnew[GS];
-    const double *Lr[NT];
+    real t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
+    real *Lnew[GS];
+    const real *Lr[NT];
     bool st[GS];
 #pragma unroll
     for (int u = 0; u < GS; ++u) {
-        const double *ar = w.arow + (ug + u) * M;
+        const real *ar = w.arow + (ug + u) * M;
         const bool ur = active && u < gs;
         st[u] = ur;
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt) {
             const int c = gl + LPR * tt;
-            t[u][tt] = (ur && c < qf) ? ar[c] : 0.0;
+            t[u][tt] = (ur && c < qf) ? ar[c] : real(0);
         }
-        dg[u] = ur ? ar[qf + u] : 0.0;
+        dg[u] = ur ? ar[qf + u] : real(0);
 #pragma unroll
-        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && ur) ? ar[qf + v] : 0.0;
-        ty[u] = ur ? -w.brow[ug + u] : 0.0;
+        for (int v = 0; v < GS; ++v) cp[u][v] = (v < u && ur) ? ar[qf + v] : real(0);
+        ty[u] = ur ? -w.brow[ug + u] : real(0);
         Lnew[u] = w.L + tri(qf + u < M ? qf + u : 0);
     }
 #pragma unroll
@@ -187,7 +193,7 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
         const int c = gl + LPR * tt;
         const bool old = active && c < qf;
         Lr[tt] = old ? w.L + tri(c) : w.L;  // dead columns: any in-bounds row
-        ivc[tt] = old ? w.inv[c] : 0.0;
+        ivc[tt] = old ? w.inv[c] : real(0);
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
@@ -197,11 +203,11 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
         for (int ln = 0; ln < lnend; ++ln) {
             const int k = LPR * tt + ln;
             const bool live = active && k < qf;
-            const double y_k = w.y[k];
-            double lsm[NT];
+            const real y_k = w.y[k];
+            real lsm[NT];
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
-            double l[GS];
+            real l[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
 #pragma unroll
@@ -228,21 +234,21 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
         for (int uf = 0; uf < GS; ++uf) {
             if (uf >= gs) break;
             const int k = qf + uf;
-            const double piv = dg[uf];
+            const real piv = dg[uf];
             if (!(piv > 1e-30)) {
                 ok = false;
                 break;
             }
-            const double dq = sqrt(piv);  // C5.2
-            const double inv_k = 1.0 / dq;
-            const double y_k = ty[uf] * inv_k;
+            const real dq = sqrt(piv);  // C5.2
+            const real inv_k = real(1) / dq;
+            const real y_k = ty[uf] * inv_k;
             psi = fma(-y_k, y_k, psi);     // C6
             w.inv[k] = inv_k;  // redundant values: every lane stores the same bits
             w.y[k] = y_k;
-            double lu[GS];
+            real lu[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) {
-                lu[u] = 0.0;
+                lu[u] = real(0);
                 if (u > uf && u < gs) {
                     lu[u] = cp[u][uf] * inv_k;
                     Lnew[u][k] = lu[u];
@@ -273,15 +279,15 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
 template <int LPR, int NT>
 __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool active, int m, int m_max) {
     const int gl = G.gl;
-    double tb[NT], ivc[NT];
+    real tb[NT], ivc[NT];
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
         const int c = gl + LPR * tt;
         const bool in = active && c < m;
-        tb[tt] = in ? w.y[c] : 0.0;
-        ivc[tt] = in ? w.inv[c] : 0.0;
+        tb[tt] = in ? w.y[c] : real(0);
+        ivc[tt] = in ? w.inv[c] : real(0);
     }
-    const double *pk = w.L + tri(m_max > 0 ? m_max - 1 : 0) + gl;  // row k, this lane's first column
+    const real *pk = w.L + tri(m_max > 0 ? m_max - 1 : 0) + gl;  // row k, this lane's first column
 #pragma unroll
     for (int tt = NT - 1; tt >= 0; --tt) {
         int ln0 = m_max - 1 - LPR * tt;
@@ -290,11 +296,11 @@ __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool
         for (int ln = ln0; ln >= 0; --ln) {
             const int k = LPR * tt + ln;
             const bool live = active && k < m;
-            double lk[NT];
+            real lk[NT];
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];  // L[k][c]; c >= k: dead
             pk -= k;
-            const double gk = G.bcast(tb[tt] * ivc[tt], ln);
+            const real gk = G.bcast(tb[tt] * ivc[tt], ln);
             if (live) w.g[k] = gk;  // broadcast value, stored by every lane of the row
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) fma_if(live, -lk[t2], gk, tb[t2]);
@@ -344,18 +350,18 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             w.hval[sl] = (int8_t)-1;  // no stale shared memory is ever decoded
         }
         for (int x = gl; x < CA; x += LPR) w.ahn[x] = 0;
-        if (gl == 0) w.dscr[0] = 0.0;
+        if (gl == 0) w.dscr[0] = real(0);
         RowBook bk{0, 0, 0, false, 0u};
         G.sync();
         {
             const bool vi = has && gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
-            const double xi = vi ? __ldg(a.val + e0i + gl) : 0.0;
+            const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
             scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr, bk);
         }
-        const double a_ii = w.dscr[0];
-        const double psi0 = a_ii;
-        double psi = psi0;
+        const real a_ii = w.dscr[0];
+        const real psi0 = a_ii;
+        real psi = psi0;
         int m = 0, steps = 0, reason = AFSAI_STOP_KMAX, fail_step = 0;
         const bool ovf0 = G.ballot(bk.ovf) != 0;  // full-warp ballot: every lane, before any && short-circuit
         bool fail = false, overflow = has && ovf0;
@@ -371,33 +377,33 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             }
             // ---- gradient: fold of each active candidate's hits (C3); no shuffles inside
             int nc = 0;
-            double ba[GS];
+            real ba[GS];
             int32_t bj[GS], bt[GS];
 #pragma unroll
-            for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = 0x7fffffff; bt[q] = -1; }
+            for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = 0x7fffffff; bt[q] = -1; }
             if (running) {
                 const int hw = bk.hw;
                 for (int aa = gl; aa < hw; aa += LPR) {
                     const int n = w.ahn[aa];  // 0: a freed slot (acc stays +0.0)
-                    double acc = 0.0;
+                    real acc = real(0);
 #pragma unroll
                     for (int h = 0; h < HC; ++h) {
                         if (h < n) {
                             const int q = w.ahq[h * CA + aa];
-                            const double gv = q < 0 ? 1.0 : w.g[q];
+                            const real gv = q < 0 ? real(1) : w.g[q];
                             acc = fma(w.hv[h * CA + aa], gv, acc);
                         }
                     }
                     c_gfma += n;
                     // branch-free insertion into the sorted top-GS list (selects)
-                    const bool cand = acc != 0.0;
+                    const bool cand = acc != real(0);
                     nc += cand;
-                    double ca = cand ? fabs(acc) : -1.0;
+                    real ca = cand ? fabs(acc) : -real(1);
                     int32_t cj = cand ? w.akey[aa] : 0x7fffffff, ct = aa;
 #pragma unroll
                     for (int q = 0; q < GS; ++q) {
                         const bool b = better(ca, cj, ba[q], bj[q]);
-                        const double ta = ba[q];
+                        const real ta = ba[q];
                         const int32_t tj = bj[q], t2 = bt[q];
                         ba[q] = b ? ca : ba[q];
                         bj[q] = b ? cj : bj[q];
@@ -432,20 +438,20 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             //      registers, the winner's lane stores its slot and row extent
             int32_t selj[GS];
             int32_t pc[GS];
-            double pv[GS];
+            real pv[GS];
             bool pvld[GS];
 #pragma unroll
             for (int u = 0; u < GS; ++u) {
                 selj[u] = 0x7fffffff;
                 pvld[u] = false;
                 pc[u] = 0;
-                pv[u] = 0.0;
+                pv[u] = real(0);
                 if (u < nsel_max) {
-                    double wa = ba[0];
+                    real wa = ba[0];
                     int32_t wj = bj[0];
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) {
-                        const double oa = G.xorv(wa, o);
+                        const real oa = G.xorv(wa, o);
                         const int32_t oj = G.xorv(wj, o);
                         if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
                     }
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     const int gn = G.bcast((int)(re[0] - rs[0]), wl);
                     pvld[u] = (u < nsel) && gl < gn;
                     pc[u] = pvld[u] ? __ldg(a.col + g0 + gl) : 0;
-                    pv[u] = pvld[u] ? __ldg(a.val + g0 + gl) : 0.0;
+                    pv[u] = pvld[u] ? __ldg(aval(a) + g0 + gl) : real(0);
                     if (won) {
                         w.sela[u] = bt[0];
 #pragma unroll
@@ -467,7 +473,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                             ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1];
                             rs[q] = rs[q + 1]; re[q] = re[q + 1];
                         }
-                        ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                        ba[GS - 1] = -real(1); bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
                     }
                 }
             }
@@ -481,8 +487,8 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             }
 #pragma unroll
             for (int u = 0; u < GS; ++u)
-                for (int c = gl; c < m + nsel; c += LPR) w.arow[u * w.M + c] = 0.0;  // what border reads
-            if (gl < nsel) w.brow[gl] = 0.0;
+                for (int c = gl; c < m + nsel; c += LPR) w.arow[u * w.M + c] = real(0);  // what border reads
+            if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             if (gl < nsel) {
                 int32_t j = selj[0];
@@ -534,7 +540,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     c_border += (unsigned long long)(q * (q - 1) / 2 + 2 * q + 1);
                 }
                 m += nsel;
-                if (!(psi > 0.0)) {
+                if (!(psi > real(0))) {
                     fail = true;
                     fail_step = k;
                     running = false;
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     a.nnz_row[orow] = 0;
                 }
             } else {
-                const double d = 1.0 / sqrt(psi);
+                const real d = real(1) / sqrt(psi);
                 int32_t *oc = a.scol + orow * a.stride;
                 double *ov = a.sval + orow * a.stride;
 #pragma unroll
@@ -641,4 +647,5 @@ SetupKernFn ls_instance(int lpr, int nt, int hc) {
 #undef AFSAI_LS_NT
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai

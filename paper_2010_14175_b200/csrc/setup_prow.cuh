@@ -21,9 +21,10 @@
 #include "setup_common.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 struct PRowState {
-    double *inv, *y, *g, *L, *arow, *brow, *dscr, *acc;
+    real *inv, *y, *g, *L, *arow, *brow, *dscr, *acc;
     int4 *pd;         // [M+1] row descriptors in ascending column order (prow_fetch)
     int64_t *rstart;  // [M] first entry of pattern row q, relative to A's base
     int64_t *rend;    // [S] end entry of the rows selected this step
@@ -40,7 +41,7 @@ __host__ __device__ inline int64_t prow_state_bytes(int H, int M, int S, int LC)
     int64_t i32 = (int64_t)H + M + 2 * S + 4 + M;
     int64_t i16 = (int64_t)LC;
     int64_t i8 = H;
-    int64_t b = dbl * 8 + 8 /* int4 alignment */ + i128 * 16 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
+    int64_t b = real_bytes(dbl) + 8 /* int4 alignment */ + i128 * 16 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
     return (b + 15) & ~int64_t(15);
 }
 
@@ -48,7 +49,7 @@ __device__ __forceinline__ PRowState carve_prow(char *base, const SetupKArgs &a)
     PRowState w;
     const int H = a.H, M = a.mmax, S = a.s;
     w.M = M;
-    double *d = reinterpret_cast<double *>(base);
+    real *d = reinterpret_cast<real *>(base);
     w.inv = d; d += M;
     w.y = d; d += M;
     w.g = d; d += M + 1;  // g[M] = 1: row i in the gradient
@@ -74,4 +75,5 @@ __device__ __forceinline__ PRowState carve_prow(char *base, const SetupKArgs &a)
     return w;
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai

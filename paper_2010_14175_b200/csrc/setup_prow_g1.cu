@@ -3,6 +3,7 @@
 #include "setup_prow_impl.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 template SetupKernFn prow_instance<1>(int nt, int nv);
 extern template SetupKernFn prow_instance<2>(int nt, int nv);
 extern template SetupKernFn prow_instance<3>(int nt, int nv);
@@ -21,4 +22,5 @@ SetupKernFn prow_kernel_for(int mmax, int s, int64_t max_row_len) {
 }
 
 int64_t prow_row_bytes(int H, int mmax, int s, int lcap) { return prow_state_bytes(H, mmax, s, lcap); }
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -2,5 +2,7 @@
 #include "setup_prow_impl.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 template SetupKernFn prow_instance<4>(int nt, int nv);
+}  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -7,6 +7,7 @@
 #include "setup_prow.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 #ifndef AFSAI_PROW_DEPTH
 #define AFSAI_PROW_DEPTH 6
@@ -53,9 +54,9 @@ __device__ __forceinline__ int hinsert_warp(int32_t *hkey, int H, int log2H, boo
 // column i (slot, value) and g~ of the row
 template <int NV>
 struct PRowFetch {
-    double v[NV];
+    real v[NV];
     int s[NV];  // acc slot (H: the spare slot); 32-bit to keep the prefetch depth in registers
-    double gq;
+    real gq;
 };
 
 // One pattern row from its descriptor pd[idx] = {first entry - e0i, list offset,
@@ -64,20 +65,20 @@ struct PRowFetch {
 // Branch-free: rows past m read row m's descriptor with no entries.  Lanes
 // without an entry fold 0 into the spare slot acc[H].
 template <int LPR, int NV>
-__device__ __forceinline__ void prow_fetch(const PRowState &w, const double *vrow, int spare, int idx, int m,
+__device__ __forceinline__ void prow_fetch(const PRowState &w, const real *vrow, int spare, int idx, int m,
                                            int gl, PRowFetch<NV> &f) {
     const bool live = idx <= m;
     const int4 d = w.pd[live ? idx : m];
     const int q = d.z & 0xffff, n = live ? (d.z >> 16) : 0;
     f.gq = w.g[q];
-    const double *vb = vrow + d.x;
+    const real *vb = vrow + d.x;
     const int16_t *lb = w.lu + d.y;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const int x = gl + LPR * v;
         const bool in = x < n;
         f.s[v] = in ? (int)lb[x] : spare;
-        f.v[v] = in ? __ldg(vb + x) : 0.0;
+        f.v[v] = in ? __ldg(vb + x) : real(0);
     }
 }
 
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
         if (gl == 0) {
             w.misc[0] = 0;  // keys inserted
             w.misc[1] = 0;  // overflow
-            w.g[M] = 1.0;   // g~_i
+            w.g[M] = real(1);   // g~_i
         }
         G.sync();
         {
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 const int64_t e = e0 + gl;
                 const bool in = e < e1i;
                 const int32_t c = in ? __ldg(a.col + e) : INT_MAX;
-                const double v = in ? __ldg(a.val + e) : 0.0;
+                const real v = in ? __ldg(aval(a) + e) : real(0);
                 if (c == i) {
                     w.dscr[0] = v;
                     // row i's descriptor: entries below the diagonal
@@ -149,9 +150,9 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             }
         }
         G.sync();
-        const double a_ii = w.dscr[0];
-        const double psi0 = a_ii;
-        double psi = psi0;
+        const real a_ii = w.dscr[0];
+        const real psi0 = a_ii;
+        real psi = psi0;
         int m = 0, steps = 0, reason = AFSAI_STOP_KMAX;
         bool fail = false, overflow = (w.misc[1] != 0) || w.misc[0] * 4 > H * 3;
         int fail_code = 0, fail_step = 0;
@@ -166,12 +167,12 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             // ---- phase G: gradient (C3) over the pattern rows in ascending column
             //      order, then row i; every acc[slot] sees the fma sequence of the
             //      storage order of its own row (bitwise symmetry, C1)
-            for (int sl = gl; sl < H; sl += LPR) w.acc[sl] = 0.0;
+            for (int sl = gl; sl < H; sl += LPR) w.acc[sl] = real(0);
             G.sync();
             {
                 PRowFetch<NV> pf[kProwDepth];
 #pragma unroll
-                const double *vrow = a.val + e0i;
+                const real *vrow = aval(a) + e0i;
                 const int spare = H;
 #pragma unroll
                 for (int d = 0; d < kProwDepth; ++d) prow_fetch<LPR, NV>(w, vrow, spare, d, m, gl, pf[d]);
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                             // spare slot H.  A lane's slots within one row are
                             // distinct columns: all loads, then all fmas, then all
                             // stores (one LDS -> DFMA -> STS chain per row).
-                            double av[NV];
+                            real av[NV];
 #pragma unroll
                             for (int v = 0; v < NV; ++v) av[v] = w.acc[pf[d].s[v]];
 #pragma unroll
@@ -200,22 +201,22 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 for (int x = 0; x <= m; ++x) c_gfma += (unsigned long long)(w.pd[x].z >> 16);
             // candidates: keys not in P with acc != 0; per-lane top-GS lists
             int nc = 0;
-            double ba[GS];
+            real ba[GS];
             int32_t bj[GS], bt[GS];
 #pragma unroll
-            for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = INT_MAX; bt[q] = -1; }
+            for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = INT_MAX; bt[q] = -1; }
             for (int sl = gl; sl < H; sl += LPR) {  // H is a multiple of LPR: no tail
                 const int32_t key = w.hkey[sl];
-                const double acc = w.acc[sl];
-                const bool cand = key != kEmpty && w.hval[sl] == kCand && acc != 0.0;
+                const real acc = w.acc[sl];
+                const bool cand = key != kEmpty && w.hval[sl] == kCand && acc != real(0);
                 nc += cand;
-                double ca = cand ? fabs(acc) : -1.0;
+                real ca = cand ? fabs(acc) : -real(1);
                 int32_t cj = cand ? key : INT_MAX, ct = sl;
                 // insertion into the sorted top-GS list with selects (no branches)
 #pragma unroll
                 for (int q = 0; q < GS; ++q) {
                     const bool b = better(ca, cj, ba[q], bj[q]);
-                    const double ta = ba[q];
+                    const real ta = ba[q];
                     const int32_t tj = bj[q], t2 = bt[q];
                     ba[q] = b ? ca : ba[q];
                     bj[q] = b ? cj : bj[q];
@@ -232,11 +233,11 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
 
             // ---- phase S: top-nsel under (|acc| desc, j asc)
             for (int u = 0; u < nsel; ++u) {
-                double wa = ba[0];
+                real wa = ba[0];
                 int32_t wj = bj[0];
 #pragma unroll
                 for (int o = LPR / 2; o > 0; o >>= 1) {
-                    const double oa = G.xorv(wa, o);
+                    const real oa = G.xorv(wa, o);
                     const int32_t oj = G.xorv(wj, o);
                     if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
                 }
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                     bj[q] = me ? bj[q + 1] : bj[q];
                     bt[q] = me ? bt[q + 1] : bt[q];
                 }
-                ba[GS - 1] = me ? -1.0 : ba[GS - 1];
+                ba[GS - 1] = me ? -real(1) : ba[GS - 1];
                 bj[GS - 1] = me ? INT_MAX : bj[GS - 1];
                 bt[GS - 1] = me ? -1 : bt[GS - 1];
             }
@@ -305,8 +306,8 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
 #pragma unroll
             for (int tt = 0; tt <= NT; ++tt)
                 if (opos[tt] >= 0) w.pd[opos[tt]] = oval[tt];
-            for (int x = gl; x < nsel * M; x += LPR) w.arow[x] = 0.0;
-            if (gl < nsel) w.brow[gl] = 0.0;
+            for (int x = gl; x < nsel * M; x += LPR) w.arow[x] = real(0);
+            if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             // list offsets of the new rows (full row lengths reserved)
             int total = 0;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 bool full = false;
                 for (int t0 = 0; t0 < total; t0 += LPR * kProwGather) {
                     int32_t cc[kProwGather];
-                    double vv[kProwGather];
+                    real vv[kProwGather];
                     int uu[kProwGather], oo[kProwGather];
 #pragma unroll
                     for (int b = 0; b < kProwGather; ++b) {
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                         const int off = t - st;
                         const int64_t e = rbu + off;
                         cc[b] = in ? __ldg(a.col + e) : INT_MAX;
-                        vv[b] = in ? __ldg(a.val + e) : 0.0;
+                        vv[b] = in ? __ldg(aval(a) + e) : real(0);
                         uu[b] = in ? u : 0;
                         oo[b] = off;
                     }
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 c_border += (unsigned long long)(q * (q - 1) / 2 + 2 * q + 1);
             }
             m += nsel;
-            if (!(psi > 0.0)) { fail = true; fail_code = AFSAI_ENOTSPD; fail_step = k; break; }
+            if (!(psi > real(0))) { fail = true; fail_code = AFSAI_ENOTSPD; fail_step = k; break; }
             PHASE(4)
 
             // ---- phase U: back-substitution (C7)
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
         }
         // ---- output: d = psi^-1/2 (Eqs. 8-9); the row sorted by column (C9) is
         //      the ord permutation
-        const double d = 1.0 / sqrt(psi);
+        const real d = real(1) / sqrt(psi);
         int32_t *oc = a.scol + orow * a.stride;
         double *ov = a.sval + orow * a.stride;
 #pragma unroll
@@ -514,4 +515,5 @@ SetupKernFn prow_instance(int nt, int nv) {
 #undef AFSAI_PROW_NV
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai

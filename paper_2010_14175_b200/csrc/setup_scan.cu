@@ -28,10 +28,11 @@
 #include "setup_common.cuh"
 
 namespace afsai {
+namespace AFSAI_PNS {
 
 // On-chip state of one row (one group), carved from dynamic shared memory.
 struct RowState {
-    double *inv, *y, *g, *L, *arow, *brow, *dscr, *hacc;
+    real *inv, *y, *g, *L, *arow, *brow, *dscr, *hacc;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *selt, *glen, *misc, *coff;
     int16_t *clist, *clen;
@@ -48,7 +49,7 @@ __host__ __device__ inline int64_t row_state_bytes(int H, int M, int S, bool hac
     int64_t i32 = (int64_t)H + M + 3 * S + 4 + CL;
     int64_t i16 = 2 * (int64_t)CL;
     int64_t i8 = H;
-    int64_t b = dbl * 8 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
+    int64_t b = real_bytes(dbl) + i64 * 8 + i32 * 4 + i16 * 2 + i8;
     return (b + 15) & ~int64_t(15);
 }
 
@@ -57,7 +58,7 @@ __device__ __forceinline__ RowState carve(char *base, const SetupKArgs &a, bool 
     const int H = a.H, M = a.mmax, S = a.s;
     w.M = M;
     w.CL = cand_cap(H);
-    double *d = reinterpret_cast<double *>(base);
+    real *d = reinterpret_cast<real *>(base);
     w.inv = d; d += M;
     w.y = d; d += M;
     w.g = d; d += M;
@@ -67,7 +68,7 @@ __device__ __forceinline__ RowState carve(char *base, const SetupKArgs &a, bool 
     w.dscr = d; d += 2;
     w.hacc = nullptr;
     if (hacc) { w.hacc = d; d += H; }
-    int64_t *l8 = reinterpret_cast<int64_t *>(d);
+    int64_t *l8 = reinterpret_cast<int64_t *>(base + real_bytes(d - reinterpret_cast<real *>(base)));
     w.gstart = l8; l8 += S;
     int32_t *ip = reinterpret_cast<int32_t *>(l8);
     w.hkey = ip; ip += H;
@@ -115,15 +116,15 @@ __device__ __forceinline__ int universe_insert(const RowState &w, const SetupKAr
 
 // Kaporin-gradient fold of one chunk of row j (C3): storage order, pattern hits only
 __device__ __forceinline__ void grad_fold(const RowState &w, int H, int log2H, int32_t i, const int32_t (&cc)[kGradChunk],
-                                          const double (&vv)[kGradChunk], double &acc, unsigned long long &nfma,
+                                          const real (&vv)[kGradChunk], real &acc, unsigned long long &nfma,
                                           unsigned long long &nent) {
-    double gv[kGradChunk];
+    real gv[kGradChunk];
     bool hit[kGradChunk];
 #pragma unroll
     for (int u = 0; u < kGradChunk; ++u) {
         const int32_t r = cc[u];
         hit[u] = false;
-        gv[u] = 1.0;
+        gv[u] = real(1);
         if (r == i) hit[u] = true;
         else if (r < i) {
             const int s2 = hfind(w.hkey, H, log2H, r);
@@ -147,12 +148,12 @@ __device__ __forceinline__ void grad_fold(const RowState &w, int H, int log2H, i
 }
 
 __device__ __forceinline__ void load_chunk(const SetupKArgs &a, int64_t eb, int cnt, int32_t (&cc)[kGradChunk],
-                                           double (&vv)[kGradChunk]) {
+                                           real (&vv)[kGradChunk]) {
 #pragma unroll
     for (int u = 0; u < kGradChunk; ++u) {
         const bool in = u < cnt;
         cc[u] = in ? __ldg(a.col + eb + u) : 0x7fffffff;
-        vv[u] = in ? __ldg(a.val + eb + u) : 0.0;
+        vv[u] = in ? __ldg(aval(a) + eb + u) : real(0);
     }
 }
 
@@ -198,18 +199,18 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
             w.misc[0] = 0;  // keys inserted
             w.misc[1] = 0;  // overflow
             w.misc[2] = 0;  // candidate list length
-            w.dscr[0] = 0.0;
+            w.dscr[0] = real(0);
         }
         G.sync();
         for (int64_t e = e0i + gl; e < e1i; e += LPR) {
             const int32_t c = a.col[e];
-            if (c == i) w.dscr[0] = a.val[e];
+            if (c == i) w.dscr[0] = aval(a)[e];
             else if (c < i) universe_insert(w, a, H, log2H, c, e0i);
         }
         G.sync();
-        const double a_ii = w.dscr[0];
-        const double psi0 = a_ii;
-        double psi = psi0;
+        const real a_ii = w.dscr[0];
+        const real psi0 = a_ii;
+        real psi = psi0;
         int m = 0, steps = 0, reason = AFSAI_STOP_KMAX;
         bool fail = false, overflow = (w.misc[1] != 0);
         int fail_code = 0, fail_step = 0;
@@ -223,14 +224,14 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
             // ---- phase G: gradient (C3), one lane per candidate, next row prefetched
             const int ncl = w.misc[2];
             int nc = 0;
-            double ba[GS];
+            real ba[GS];
             int32_t bj[GS], bt[GS];
 #pragma unroll
-            for (int q = 0; q < GS; ++q) { ba[q] = -1.0; bj[q] = 0x7fffffff; bt[q] = -1; }
+            for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = 0x7fffffff; bt[q] = -1; }
             {
                 int t = gl;
                 int32_t ncc[kGradChunk];
-                double nvv[kGradChunk];
+                real nvv[kGradChunk];
                 int64_t neb = 0;
                 int nlen = 0;
                 if (t < ncl) {
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                 }
                 while (t < ncl) {
                     int32_t cc[kGradChunk];
-                    double vv[kGradChunk];
+                    real vv[kGradChunk];
 #pragma unroll
                     for (int u = 0; u < kGradChunk; ++u) { cc[u] = ncc[u]; vv[u] = nvv[u]; }
                     const int64_t eb = neb;
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                         nlen = w.clen[t];
                         load_chunk(a, neb, nlen, ncc, nvv);
                     }
-                    double acc = 0.0;
+                    real acc = real(0);
                     grad_fold(w, H, log2H, i, cc, vv, acc, c_gfma, c_gent);
                     for (int off = kGradChunk; off < len && cc[kGradChunk - 1] < i; off += kGradChunk) {
                         load_chunk(a, eb + off, len - off, cc, vv);
@@ -260,16 +261,16 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                     }
                     const int sl = w.clist[tc];
                     if (use_hacc) w.hacc[sl] = acc;
-                    if (acc != 0.0) {
+                    if (acc != real(0)) {
                         ++nc;
                         if (!use_hacc) {
-                            double ca = fabs(acc);
+                            real ca = fabs(acc);
                             int32_t cj = w.hkey[sl];
                             int32_t ct = tc;
 #pragma unroll
                             for (int q = 0; q < GS; ++q) {
                                 if (better(ca, cj, ba[q], bj[q])) {
-                                    const double ta = ba[q];
+                                    const real ta = ba[q];
                                     const int32_t tj = bj[q], t2 = bt[q];
                                     ba[q] = ca; bj[q] = cj; bt[q] = ct;
                                     ca = ta; cj = tj; ct = t2;
@@ -287,11 +288,11 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
             // ---- phase S: top-nsel under the total order (|acc| desc, j asc)
             if (!use_hacc) {
                 for (int u = 0; u < nsel; ++u) {
-                    double wa = ba[0];
+                    real wa = ba[0];
                     int32_t wj = bj[0];
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) {
-                        const double oa = G.xorv(wa, o);
+                        const real oa = G.xorv(wa, o);
                         const int32_t oj = G.xorv(wj, o);
                         if (better(oa, oj, wa, wj)) { wa = oa; wj = oj; }
                     }
@@ -300,25 +301,25 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                         w.selt[u] = bt[0];
 #pragma unroll
                         for (int q = 0; q + 1 < GS; ++q) { ba[q] = ba[q + 1]; bj[q] = bj[q + 1]; bt[q] = bt[q + 1]; }
-                        ba[GS - 1] = -1.0; bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
+                        ba[GS - 1] = -real(1); bj[GS - 1] = 0x7fffffff; bt[GS - 1] = -1;
                     }
                 }
             } else {
                 // s > GS: nsel rounds of group argmax over the candidate list
                 for (int u = 0; u < nsel; ++u) {
-                    double xa = -1.0;
+                    real xa = -real(1);
                     int32_t xj = 0x7fffffff, xt = -1;
                     for (int t = gl; t < ncl; t += LPR) {
                         const int sl = w.clist[t];
                         if (w.hval[sl] != kCand) continue;
-                        const double aa = fabs(w.hacc[sl]);
-                        if (aa == 0.0) continue;
+                        const real aa = fabs(w.hacc[sl]);
+                        if (aa == real(0)) continue;
                         const int32_t j = w.hkey[sl];
                         if (better(aa, j, xa, xj)) { xa = aa; xj = j; xt = t; }
                     }
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) {
-                        const double oa = G.xorv(xa, o);
+                        const real oa = G.xorv(xa, o);
                         const int32_t oj = G.xorv(xj, o);
                         const int32_t ot = G.xorv(xt, o);
                         if (better(oa, oj, xa, xj)) { xa = oa; xj = oj; xt = ot; }
@@ -366,8 +367,8 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                 if (gl == 0) w.misc[2] = wr;
             }
             // zero the gathered rows
-            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = 0.0;
-            if (gl < nsel) w.brow[gl] = 0.0;
+            for (int x = gl; x < nsel * w.M; x += LPR) w.arow[x] = real(0);
+            if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             PHASE(2)
 
@@ -381,12 +382,12 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                     while (off >= w.glen[u]) { off -= w.glen[u]; ++u; }
                     const int64_t e = w.gstart[u] + off;
                     const int32_t c = __ldg(a.col + e);
-                    if (c == i) w.brow[u] = __ldg(a.val + e);
+                    if (c == i) w.brow[u] = __ldg(aval(a) + e);
                     else if (c < i) {
                         const int sl = universe_insert(w, a, H, log2H, c, e0i);
                         if (sl >= 0) {
                             const int st = w.hval[sl];
-                            if (st >= 0 && st <= m + u) w.arow[u * w.M + st] = __ldg(a.val + e);
+                            if (st >= 0 && st <= m + u) w.arow[u * w.M + st] = __ldg(aval(a) + e);
                         }
                     }
                 }
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
                 c_border += (unsigned long long)(q * (q - 1) / 2 + 2 * q + 1);
             }
             m += nsel;
-            if (!(psi > 0.0)) { fail = true; fail_code = AFSAI_ENOTSPD; fail_step = k; break; }
+            if (!(psi > real(0))) { fail = true; fail_code = AFSAI_ENOTSPD; fail_step = k; break; }
             PHASE(4)
 
             // ---- phase U: back-substitution
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
             continue;
         }
         // ---- output: d = psi^-1/2 (Eqs. 8-9), row sorted by column (C9)
-        const double d = 1.0 / sqrt(psi);
+        const real d = real(1) / sqrt(psi);
         int32_t *oc = a.scol + orow * a.stride;
         double *ov = a.sval + orow * a.stride;
 #pragma unroll
@@ -491,9 +492,11 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_ker
     }
 }
 
+}  // namespace AFSAI_PNS
 }  // namespace afsai
 
 namespace afsai {
+namespace AFSAI_PNS {
 // ---------------------------------------------------------------- host side
 template <int LPR, int NT>
 static SetupKernFn scan_gs(int gs) {
@@ -529,4 +532,5 @@ int64_t scan_row_bytes(int H, int mmax, int s) {
     const int gs = s < kMaxGroup ? s : kMaxGroup;
     return row_state_bytes(H, mmax, s, s > gs);
 }
+}  // namespace AFSAI_PNS
 }  // namespace afsai

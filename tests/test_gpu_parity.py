@@ -25,9 +25,9 @@ def ctx():
     c.close()
 
 
-def gpu_setup(ctx, A, nsteps, s, eps=0.0, cap=1 << 30):
+def gpu_setup(ctx, A, nsteps, s, eps=0.0, cap=1 << 30, precision="fp64"):
     from paper_2010_14175_b200.api import DeviceCSR, Factor
-    F = Factor(ctx, DeviceCSR.from_numpy(A), nsteps, s, eps, cap)
+    F = Factor(ctx, DeviceCSR.from_numpy(A), nsteps, s, eps, cap, precision=precision)
     return F
 
 
@@ -110,6 +110,61 @@ def test_setup_parity(ctx, name, make, k, s, eps, cap):
     if name.startswith("arrow"):
         assert np.diff(T.rowptr).max() > 2048, "the long-row transpose path was not exercised"
     F.close()
+
+
+@pytest.mark.parametrize("name,make,k,s,eps,cap", CASES, ids=[c[0] for c in CASES])
+def test_setup_parity_fp32(ctx, name, make, k, s, eps, cap):
+    """The single-precision set-up (P:953-965; afsai::sp kernels) against the fp32
+    oracle: bitwise G (= double(G_s)), identical trace, G^T bitwise."""
+    A = make()
+    F = gpu_setup(ctx, A, k, s, eps, cap, precision="fp32")
+    G = host_csr(F)
+    ref = oracle.setup(A, k, s, eps, cap, precision="fp32")
+    Gr = ref.to_csr(A.n)
+    assert np.array_equal(G.rowptr, Gr.rowptr) and np.array_equal(G.col, Gr.col)
+    assert np.array_equal(G.val.view(np.int64), Gr.val.view(np.int64)), name
+    st, rs = F.trace()
+    assert np.array_equal(st.cpu().numpy(), ref.steps) and np.array_equal(rs.cpu().numpy(), ref.reason)
+    assert F.stats()["value_bytes"] == 4
+    T = host_csr(F, 1)
+    Tr = oracle.transpose(Gr)
+    assert np.array_equal(T.col, Tr.col) and np.array_equal(T.val.view(np.int64), Tr.val.view(np.int64))
+    F.close()
+
+
+@pytest.mark.parametrize("env", [{"AFSAI_TABLE": "64"}, {"AFSAI_PROW": "0"}, {"AFSAI_HITS": "0"}],
+                         ids=["retry_from_64", "scan_kernel_fe", "scan_kernel_stencil"])
+def test_setup_parity_fp32_plans(ctx, env, monkeypatch):
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    for A, k, s, cap in [(ai.fe_elasticity(4), 30, 3, 100), (ai.hetero_poisson3d(12), 20, 2, 1 << 30)]:
+        F = gpu_setup(ctx, A, k, s, 0.0, cap, precision="fp32")
+        G = host_csr(F)
+        Gr = oracle.setup(A, k, s, 0.0, cap, precision="fp32").to_csr(A.n)
+        assert np.array_equal(G.col, Gr.col) and np.array_equal(G.val.view(np.int64), Gr.val.view(np.int64))
+        F.close()
+
+
+@pytest.mark.parametrize("make,k,s,cap", [(lambda: ai.poisson3d(16), 20, 2, 1 << 30),
+                                          (lambda: ai.hetero_poisson3d(12), 20, 2, 1 << 30),
+                                          (lambda: ai.fe_elasticity(6), 30, 3, 100)])
+def test_pcg_fp32_setup(ctx, make, k, s, cap):
+    """PCG with the fp32-set-up G needs <= 1.2x the iterations of the fp64 G,
+    and its count is within 1 of the oracle PCG on the fp32 oracle's G."""
+    A = make()
+    b, _ = ai.rhs_for(A)
+    bd = torch.from_numpy(b).cuda()
+    F64 = gpu_setup(ctx, A, k, s, 0.0, cap)
+    F32 = gpu_setup(ctx, A, k, s, 0.0, cap, precision="fp32")
+    _, r64 = F64.pcg(bd, tol=1e-8, max_iters=5000)
+    _, r32 = F32.pcg(bd, tol=1e-8, max_iters=5000)
+    assert r64["converged"] and r32["converged"]
+    assert r32["iters"] <= int(np.ceil(1.2 * r64["iters"])), (r32["iters"], r64["iters"])
+    G, Gt, _ = oracle.setup_full(A, k, s, 0.0, cap, precision="fp32")
+    pr = oracle.pcg(A, G, Gt, b, tol=1e-8, max_iters=5000)
+    assert abs(r32["iters"] - pr.iters) <= 1
+    F64.close()
+    F32.close()
 
 
 @pytest.mark.parametrize("env", [{"AFSAI_TABLE": "64"}, {"AFSAI_PROW": "0"}, {"AFSAI_NOPROBE": "1"}],
