@@ -85,6 +85,11 @@ typedef struct {
     int32_t precision;     /* set-up arithmetic: AFSAI_PREC_FP64 (0, default) or
                               AFSAI_PREC_FP32 (§4.3: A_s = single(A),
                               the set-up in fp32, G = double(G_s); apply/PCG stay fp64) */
+    int32_t halo_k;        /* multi-GPU set-up halo: 0 (default) = the exact halo, G bitwise the
+                              1-GPU G; 1..3 = the paper's bounded communication:
+                              rank p sets up on A[I_p, I_p], I_p = the row stripes q <= p with
+                              (A-hat^k)_pq != 0 (A-hat: the block pattern of A over ranks),
+                              entries outside are zero -- G changes with k.  Ignored on 1 GPU. */
 } afsai_params_t;
 #define AFSAI_PREC_FP64 0
 #define AFSAI_PREC_FP32 1
@@ -121,8 +126,10 @@ typedef struct {
     int64_t max_universe;        /* largest candidate+pattern set of a row (table keys) */
     int32_t plan;                /* kernel plan of the main pass: AFSAI_PLAN_*        */
     int32_t lanes_per_row;       /* lanes of a warp working on one row               */
-    int32_t value_bytes;         /* 8: fp64 set-up; 4: fp32 set-up (AFSAI_SETUP_FP32) */
+    int32_t value_bytes;         /* 8: fp64 set-up; 4: fp32 set-up (AFSAI_PREC_FP32)   */
     int32_t reserved;
+    int64_t halo_bytes;          /* multi-GPU: bytes of A rows received for the set-up halo */
+    int64_t halo_mask;           /* multi-GPU: bit q = the set-up used rank q's stripe      */
 } afsai_setup_stats_t;
 #define AFSAI_PLAN_LOCKSTEP 0    /* hit lists, several rows per warp in lockstep (stencils) */
 #define AFSAI_PLAN_PROW 1        /* pattern-row folds (long rows, FE)                        */

@@ -241,3 +241,48 @@ def setup_full(A, nsteps, s, eps=0.0, max_row_nnz=1 << 30, threads=None, precisi
     res = setup(A, nsteps, s, eps, max_row_nnz, threads=threads, precision=precision)
     G = res.to_csr(A.n)
     return G, transpose(G), res
+
+
+# ------------------------------------------------------------------ bounded communication
+def comm_matrix(A, bounds):
+    """A-hat: n_p x n_p boolean, A-hat[p, q] = 1 iff the block of A
+    with rows in stripe p and columns in stripe q holds a nonzero.  Stripe q = rows
+    [bounds[q], bounds[q+1])."""
+    bounds = np.asarray(bounds, dtype=np.int64)
+    npr = len(bounds) - 1
+    rows = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.rowptr))
+    po = np.searchsorted(bounds, rows, side="right") - 1
+    qo = np.searchsorted(bounds, A.col.astype(np.int64), side="right") - 1
+    H = np.zeros((npr, npr), dtype=bool)
+    H[po, qo] = True
+    return H
+
+
+def stripes_used(Ahat, p, k):
+    """The stripes q <= p with (A-hat^k)[p, q] != 0: G-hat <= lower(A-hat^k),
+    by k boolean matrix products."""
+    R = np.eye(Ahat.shape[0], dtype=bool)
+    for _ in range(k):
+        R = (R.astype(np.int64) @ Ahat.astype(np.int64)) > 0
+    return [q for q in range(p + 1) if R[p, q]]
+
+
+def setup_bounded(A, bounds, p, k, nsteps, s, eps=0.0, max_row_nnz=1 << 30, precision="fp64"):
+    """The rows of stripe p of the bounded-communication set-up: aFSAI on
+    the principal submatrix A[I_p, I_p], I_p = the union of the stripes q <= p with
+    (A-hat^k)[p, q] != 0; every entry of A outside I_p x I_p is zero.  (Rows outside
+    I_p keep only their diagonal: they are never read.)"""
+    from afsai_inputs import CSR
+    bounds = np.asarray(bounds, dtype=np.int64)
+    used = stripes_used(comm_matrix(A, bounds), p, k)
+    inI = np.zeros(A.n, dtype=bool)
+    for q in used:
+        inI[bounds[q]:bounds[q + 1]] = True
+    rows = np.repeat(np.arange(A.n, dtype=np.int64), np.diff(A.rowptr))
+    keep = (inI[rows] & inI[A.col]) | (rows == A.col)
+    cnt = np.bincount(rows[keep], minlength=A.n)
+    rp = np.zeros(A.n + 1, dtype=np.int64)
+    np.cumsum(cnt, out=rp[1:])
+    T = CSR(A.n, rp, A.col[keep].astype(np.int32), A.val[keep].astype(np.float64), "A_Ip")
+    res = setup(T, nsteps, s, eps, max_row_nnz, rows=np.arange(bounds[p], bounds[p + 1]), precision=precision)
+    return res, used

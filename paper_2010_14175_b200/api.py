@@ -94,12 +94,13 @@ class Factor:
     """G (and G^T) of one afsai_setup call."""
 
     def __init__(self, ctx: Context, A: DeviceCSR, nsteps: int, s: int, eps: float = 0.0,
-                 max_row_nnz: int = 1 << 30, precision: str = "fp64"):
-        """precision="fp32": the single-precision set-up; G is fp64 either way."""
+                 max_row_nnz: int = 1 << 30, precision: str = "fp64", halo_k: int = 0):
+        """precision="fp32": the single-precision set-up; G is fp64 either way.
+        halo_k (multi-GPU): 0 = exact set-up halo; 1..3 = bounded communication A-hat^k."""
         self.ctx = ctx
         self.A = A
         self.h = capi.afsai_setup(ctx.h, A.c(), nsteps, s, eps, min(max_row_nnz, 2**31 - 1),
-                                  capi.PRECISIONS[precision])
+                                  capi.PRECISIONS[precision], halo_k)
 
     @property
     def nnz(self):

@@ -39,7 +39,7 @@ class afsai_csr_t(ctypes.Structure):
 
 class afsai_params_t(ctypes.Structure):
     _fields_ = [("nsteps", ctypes.c_int32), ("s", ctypes.c_int32), ("eps", ctypes.c_double),
-                ("max_row_nnz", ctypes.c_int32), ("precision", ctypes.c_int32)]
+                ("max_row_nnz", ctypes.c_int32), ("precision", ctypes.c_int32), ("halo_k", ctypes.c_int32)]
 
 
 class afsai_status_t(ctypes.Structure):
@@ -56,7 +56,8 @@ class afsai_setup_stats_t(ctypes.Structure):
                 ("table_size", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32), ("retried_rows", ctypes.c_int32),
                 ("halo_rows", ctypes.c_int32), ("phase_cycles", ctypes.c_int64 * 7),
                 ("max_universe", ctypes.c_int64), ("plan", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
-                ("value_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("value_bytes", ctypes.c_int32), ("reserved", ctypes.c_int32), ("halo_bytes", ctypes.c_int64),
+                ("halo_mask", ctypes.c_int64)]
     PLANS = {0: "lockstep", 1: "prow", 2: "hits", 3: "scan"}
 
     PHASES = ["prologue", "gradient", "select", "gather", "border", "backsub", "output"]
@@ -192,8 +193,9 @@ AFSAI_PREC_FP64, AFSAI_PREC_FP32 = 0, 1
 PRECISIONS = {"fp64": AFSAI_PREC_FP64, "fp32": AFSAI_PREC_FP32}
 
 
-def afsai_setup(ctx, A: afsai_csr_t, nsteps: int, s: int, eps: float, max_row_nnz: int, precision: int = 0):
-    p = afsai_params_t(nsteps, s, eps, max_row_nnz, precision)
+def afsai_setup(ctx, A: afsai_csr_t, nsteps: int, s: int, eps: float, max_row_nnz: int, precision: int = 0,
+                halo_k: int = 0):
+    p = afsai_params_t(nsteps, s, eps, max_row_nnz, precision, halo_k)
     f = ctypes.c_void_p()
     st = afsai_status_t()
     rc = lib().afsai_setup(ctx, ctypes.byref(A), ctypes.byref(p), ctypes.byref(f), ctypes.byref(st))

@@ -430,6 +430,132 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
     return AFSAI_OK;
 }
 
+// ---- bounded-communication set-up
+// owner of a global row / column: the rank q with bounds[q] <= x < bounds[q+1]
+__device__ __forceinline__ int owner_of(const int64_t *bounds, int np, int64_t x) {
+    int lo = 0, hi = np;  // bounds[lo] <= x < bounds[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (bounds[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// this rank's row of the communication matrix A-hat: bit q set iff a local row has
+// a column owned by rank q
+__global__ void comm_row_kernel(const int64_t *rowptr, const int32_t *col, int64_t base, int64_t n_rows,
+                                const int64_t *bounds, int np, unsigned long long *mask) {
+    unsigned long long m = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t e = rowptr[r] - base; e < rowptr[r + 1] - base; ++e) m |= 1ull << owner_of(bounds, np, col[e]);
+    atomicOr(mask, m);
+}
+
+// N_p = { q <= p : (A-hat^k)_pq != 0 } as a bit mask.  A-hat is gathered from all
+// ranks; its diagonal is nonzero (diagonal entries), so A-hat^k's pattern is the
+// set of ranks reachable from p in at most k steps (a few boolean products).
+static int comm_neighbours(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<int64_t> &bounds, int k,
+                           uint64_t *nmask, afsai_status_t *status) {
+    cudaStream_t st = ctx->stream;
+    const int np = ctx->nranks;
+    if (np > 64) return set_status(status, AFSAI_ELIMIT, "the bounded-communication set-up supports <= 64 ranks");
+    DevBuf db, dm;
+    AFSAI_CUDA_TRY(db.alloc((np + 1) * sizeof(int64_t), st));
+    AFSAI_CUDA_TRY(dm.alloc(sizeof(unsigned long long), st));
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(db.p, bounds.data(), (np + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    AFSAI_CUDA_TRY(cudaMemsetAsync(dm.p, 0, sizeof(unsigned long long), st));
+    comm_row_kernel<<<grid_stream(ctx), 256, 0, st>>>(A.rowptr, A.col, A.base, A.n_rows, db.as<int64_t>(), np,
+                                                      dm.as<unsigned long long>());
+    ctx->launches += 1;
+    unsigned long long mine = 0;
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(&mine, dm.p, sizeof mine, cudaMemcpyDeviceToHost, st));
+    AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int64_t> rows;  // A-hat, one bit row per rank
+    int rc = allgather_i64(ctx, (int64_t)mine, rows, status);
+    if (rc) return rc;
+    uint64_t reach = 1ull << ctx->rank;
+    for (int t = 0; t < k; ++t) {
+        uint64_t nx = reach;
+        for (int q = 0; q < np; ++q)
+            if ((reach >> q) & 1ull) nx |= (uint64_t)rows[q];
+        reach = nx;
+    }
+    const uint64_t lower = ctx->rank == 63 ? ~0ull : ((2ull << ctx->rank) - 1ull);
+    *nmask = reach & lower;
+    return AFSAI_OK;
+}
+
+// keep entry (r, c) of the extended rows iff owner(r) and owner(c) are in nmask:
+// X becomes A[I_p, I_p] (rows of the other stripes empty; they are never read)
+__global__ void stripe_count_kernel(const int64_t *rowptr, const int32_t *col, int64_t base, int64_t n_rows,
+                                    int64_t row_begin, const int64_t *bounds, int np, unsigned long long nmask,
+                                    int32_t *cnt) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        int c = 0;
+        if ((nmask >> owner_of(bounds, np, r + row_begin)) & 1ull)
+            for (int64_t e = rowptr[r] - base; e < rowptr[r + 1] - base; ++e)
+                c += (int)((nmask >> owner_of(bounds, np, col[e])) & 1ull);
+        cnt[r] = c;
+    }
+}
+
+__global__ void stripe_fill_kernel(const int64_t *rowptr, const int32_t *col, const double *val, int64_t base,
+                                   int64_t n_rows, int64_t row_begin, const int64_t *bounds, int np,
+                                   unsigned long long nmask, const int64_t *orp, int32_t *ocol, double *oval) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        if (!((nmask >> owner_of(bounds, np, r + row_begin)) & 1ull)) continue;
+        int64_t o = orp[r];
+        for (int64_t e = rowptr[r] - base; e < rowptr[r + 1] - base; ++e)
+            if ((nmask >> owner_of(bounds, np, col[e])) & 1ull) {
+                ocol[o] = col[e];
+                oval[o] = val[e];
+                ++o;
+            }
+    }
+}
+
+static int truncate_to_stripes(afsai_ctx_t ctx, const DeviceCsr &X, const std::vector<int64_t> &bounds,
+                               uint64_t nmask, DeviceCsr *T, afsai_status_t *status) {
+    cudaStream_t st = ctx->stream;
+    const int np = ctx->nranks;
+    const int64_t n = X.n_rows;
+    DevBuf db, cnt, tiles;
+    AFSAI_CUDA_TRY(db.alloc((np + 1) * sizeof(int64_t), st));
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(db.p, bounds.data(), (np + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    AFSAI_CUDA_TRY(cnt.alloc(std::max<int64_t>(n, 1) * sizeof(int32_t), st));
+    AFSAI_CUDA_TRY(tiles.alloc(scan_tmp_elems(n) * sizeof(int64_t) + 16, st));
+    AFSAI_CUDA_TRY(T->b_rowptr.alloc((n + 1) * sizeof(int64_t), st));
+    const int grid = grid_stream(ctx);
+    stripe_count_kernel<<<grid, 256, 0, st>>>(X.rowptr, X.col, X.base, n, X.row_begin, db.as<int64_t>(), np, nmask,
+                                              cnt.as<int32_t>());
+    ctx->launches += 1;
+    AFSAI_CUDA_TRY(exclusive_scan(cnt.as<int32_t>(), n, T->b_rowptr.as<int64_t>(), tiles.as<int64_t>(), st,
+                                  &ctx->launches));
+    int64_t nnz = 0;
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(&nnz, T->b_rowptr.as<int64_t>() + n, sizeof nnz, cudaMemcpyDeviceToHost, st));
+    AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+    AFSAI_CUDA_TRY(T->b_col.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), st));
+    AFSAI_CUDA_TRY(T->b_val.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st));
+    stripe_fill_kernel<<<grid, 256, 0, st>>>(X.rowptr, X.col, X.val, X.base, n, X.row_begin, db.as<int64_t>(), np,
+                                             nmask, T->b_rowptr.as<int64_t>(), T->b_col.as<int32_t>(),
+                                             T->b_val.as<double>());
+    ctx->launches += 1;
+    AFSAI_CUDA_TRY(cudaGetLastError());
+    T->rowptr = T->b_rowptr.as<int64_t>();
+    T->col = T->b_col.as<int32_t>();
+    T->val = T->b_val.as<double>();
+    T->base = 0;
+    T->n_rows = n;
+    T->n_cols = X.n_cols;
+    T->row_begin = X.row_begin;
+    T->nnz = nnz;
+    T->staged = true;
+    return AFSAI_OK;
+}
+
 int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p, afsai_factor_t *out,
                afsai_status_t *status) {
     cudaStream_t st = ctx->stream;
@@ -486,11 +612,35 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
     // exact set-up halo: rows [b - kmax*beta, b)
     const int64_t b = A.row_begin, e = b + A.n_rows;
     const int64_t reach = std::min<int64_t>(b, (int64_t)p->nsteps * D->betaA);
-    const int64_t lo = b - reach;
+    int64_t lo = b - reach;
+    // bounded-communication set-up: G-hat <= lower(A-hat^k); the
+    // rank gathers the stripes q <= p with (A-hat^k)_pq != 0 and sets up on the
+    // principal submatrix A[I_p, I_p] of their rows (entries outside are zero)
+    uint64_t nmask = 0;
+    if (p->halo_k > 0) {
+        rc = agree(ctx, comm_neighbours(ctx, A, D->bounds, p->halo_k, &nmask, status), status);
+        if (rc) return fail(rc);
+        int q0 = 0;
+        while (!((nmask >> q0) & 1ull)) ++q0;
+        lo = D->bounds[q0];
+    }
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
     DeviceCsr X;
     rc = agree(ctx, gather_halo(ctx, A, D->bounds, lo, &X, status), status);
     if (rc) return fail(rc);
+    int64_t halo_entries = 0;
+    {
+        int64_t h0 = 0;
+        AFSAI_CUDA_TRY(cudaMemcpyAsync(&h0, X.rowptr + (b - lo), sizeof h0, cudaMemcpyDeviceToHost, st));
+        AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+        halo_entries = h0;  // entries of the received rows [lo, b)
+    }
+    if (p->halo_k > 0) {
+        DeviceCsr T;
+        rc = agree(ctx, truncate_to_stripes(ctx, X, D->bounds, nmask, &T, status), status);
+        if (rc) return fail(rc);
+        X = std::move(T);
+    }
 #ifdef AFSAI_BOUNDS_CHECK
     {   // debug build: the gathered halo-extended matrix must be a valid CSR
         int64_t ml = 0;
@@ -504,6 +654,8 @@ int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p,
 #endif
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
     F->stats.halo_rows = (int32_t)(b - lo);
+    F->stats.halo_bytes = halo_entries * (int64_t)(sizeof(int32_t) + sizeof(double)) + (b - lo) * 4;
+    F->stats.halo_mask = (int64_t)nmask;
     rc = agree(ctx, block_rows_to_G(ctx, X, lo, e, b, A.n_rows, p, maxlen, F, status), status);
     if (rc) return fail(rc);
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[3], st));

@@ -654,9 +654,10 @@ int afsai_setup(afsai_ctx_t ctx, const afsai_csr_t *A, const afsai_params_t *p, 
         A->n_cols >= (int64_t)INT32_MAX || (A->n_rows > 0 && (!A->rowptr || !A->col || !A->val)))
         return set_status(status, AFSAI_EINVAL, "bad matrix sizes or null arrays");
     if (p->nsteps < 0 || p->s < 1 || p->s > AFSAI_MAX_S || !(p->eps >= 0.0 && p->eps < 1.0) || p->max_row_nnz < 1 ||
-        (p->precision != AFSAI_PREC_FP64 && p->precision != AFSAI_PREC_FP32))
+        (p->precision != AFSAI_PREC_FP64 && p->precision != AFSAI_PREC_FP32) || p->halo_k < 0 || p->halo_k > 64)
         return set_status(status, AFSAI_EINVAL,
-                          "params out of range (nsteps>=0, 1<=s<=16, 0<=eps<1, max_row_nnz>=1, precision 0|1)");
+                          "params out of range (nsteps>=0, 1<=s<=16, 0<=eps<1, max_row_nnz>=1, precision 0|1, "
+                          "0<=halo_k<=64)");
     const int64_t mmax64 = std::min<int64_t>((int64_t)p->nsteps * p->s, (int64_t)p->max_row_nnz - 1);
     if (mmax64 > AFSAI_MAX_MMAX)
         return set_status(status, AFSAI_ELIMIT, "min(nsteps*s, max_row_nnz-1) exceeds AFSAI_MAX_MMAX (128)");

@@ -62,6 +62,30 @@ for name, A, k, s, cap in cases:
                      "iters_N": rep["iters"], "iters_oracle": pr.iters, "true_rel_res": rep["true_rel_res"],
                      "halo_rows": stats["halo_rows"], "ms_total": stats["ms_total"], "ms_halo": stats["ms_halo"]}
     F.close()
+# bounded-communication set-up: halo_k = 1, 2 against the oracle on A[I_p, I_p]
+for name, A, k, s, cap in [("poisson3d_24", ai.poisson3d(24), 20, 2, 1000), ("fe_7", ai.fe_elasticity(7), 30, 3, 100)]:
+    n = A.n
+    bounds = [n * q // world for q in range(world + 1)]
+    b, e = bounds[rank], bounds[rank + 1]
+    bvec, _ = ai.rhs_for(A)
+    for hk in (1, 2):
+        ref, used = oracle.setup_bounded(A, bounds, rank, hk, k, s, 0.0, cap)
+        F = Factor(ctx, DeviceCSR.from_numpy(A, row_begin=b, n_rows=e - b), k, s, 0.0, cap, halo_k=hk)
+        rp, ci, v = (t.cpu().numpy() for t in F.G())
+        ok = True
+        for t in range(e - b):
+            c0, v0 = ref.row(t)
+            if not (np.array_equal(ci[rp[t]:rp[t + 1]], c0) and
+                    np.array_equal(v[rp[t]:rp[t + 1]].view(np.int64), v0.view(np.int64))):
+                ok = False
+                break
+        x, rep = F.pcg(torch.from_numpy(bvec[b:e].copy()).cuda(), tol=1e-8, max_iters=5000)
+        st = F.stats()
+        mask = [q for q in range(world) if (st["halo_mask"] >> q) & 1]
+        results[f"{name}_halo_k{hk}"] = {"G_bitwise_vs_oracle": bool(ok), "stripes": mask, "oracle_stripes": used,
+                                         "iters_N": rep["iters"], "converged": bool(rep["converged"]),
+                                         "halo_rows": st["halo_rows"], "halo_bytes": st["halo_bytes"]}
+        F.close()
 # error agreement: row n-1 has a tiny diagonal (psi < 0 at step 1 on the last rank only)
 B = ai.poisson3d(12)
 val = B.val.copy()
@@ -88,7 +112,9 @@ dist.all_gather_object(allr, results)
 if rank == 0:
     ok = all(r[c]["G_bitwise_vs_oracle"] and r[c]["Gt_bitwise_vs_oracle"] and r[c]["apply_within_bound_vs_oracle"]
              and abs(r[c]["iters_N"] - r[c]["iters_oracle"]) <= 1 and r[c]["true_rel_res"] <= 1e-7
-             for r in allr for c in r if c != "error_agreement")
+             for r in allr for c in r if c != "error_agreement" and "_halo_k" not in c)
+    ok = ok and all(r[c]["G_bitwise_vs_oracle"] and r[c]["converged"] and r[c]["stripes"] == r[c]["oracle_stripes"]
+                    for r in allr for c in r if "_halo_k" in c)
     ok = ok and all(r["error_agreement"]["ok"] for r in allr) and allr[0]["error_agreement"]["oracle_code"] == 2
     print(json.dumps({"world": world, "ok": ok, "ranks": allr}, indent=1))
 dist.destroy_process_group()

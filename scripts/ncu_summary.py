@@ -31,12 +31,14 @@ tot = sum(float(b.replace(",", "") or 0) for _, b in items)
 print("stall reasons (share of PC samples):")
 for a, b in sorted(items, key=lambda t: -float(t[1].replace(",", "") or 0))[:10]:
     print(f"  {a.replace('smsp__pcsamp_warps_issue_stalled_', ''):30s} {100 * float(b.replace(',', '')) / tot:6.2f}%")
-for key in ("inst_executed", "sm__sass_thread_inst_executed_op_dfma_pred_on.sum",
-            "dram__bytes_read.sum", "dram__bytes_write.sum"):
-    for a, b in zip(h, v):
-        if a == key or a.startswith(key):
-            print(f"  {a:45s} {b}")
-            break
+# executed counts (exact metric names; the .peak_sustained variants are capacities, not counts)
+print("executed counters:")
+for a, b in zip(h, v):
+    if (a in ("smsp__inst_executed.sum", "sm__inst_executed.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+              "gpu__time_duration.sum")
+            or (("dfma" in a or "fp64" in a or "pipe_fma" in a or "dmul" in a or "dadd" in a)
+                and (a.endswith(".sum") or "pct_of_peak_sustained" in a) and "peak_sustained." not in a)):
+        print(f"  {a:70s} {b}")
 if len(sys.argv) > 5:
     print("top source lines:")
     out = subprocess.run([sys.executable, __file__.replace("ncu_summary.py", "sass_lines.py"), sys.argv[3],

@@ -40,13 +40,29 @@ def test_library_exports_every_declared_symbol(lib):
         assert hasattr(lib, n), n
 
 
-def test_struct_layouts_match_header(lib):
+def test_struct_layouts_match_header(lib, tmp_path):
+    """Every struct of include/afsai.h has the ctypes mirror's size and field offsets
+    (measured by a C program compiled against the header)."""
+    import subprocess
     from paper_2010_14175_b200 import capi
-    # sizes implied by the header (x86-64 SysV alignment)
-    assert ctypes.sizeof(capi.afsai_csr_t) == 7 * 8
-    assert ctypes.sizeof(capi.afsai_params_t) == 24
-    assert ctypes.sizeof(capi.afsai_status_t) == 4 + 4 + 8 + 4 + 160 + 4
-    assert ctypes.sizeof(capi.afsai_pcg_report_t) == 8 + 4 * 8
+    structs = {"afsai_csr_t": capi.afsai_csr_t, "afsai_params_t": capi.afsai_params_t,
+               "afsai_status_t": capi.afsai_status_t, "afsai_setup_stats_t": capi.afsai_setup_stats_t,
+               "afsai_pcg_report_t": capi.afsai_pcg_report_t}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "afsai.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(((a, b), int(c)) for a, b, c in (ln.split() for ln in subprocess.check_output([str(exe)], text=True).splitlines()))
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[(name, f)] == getattr(cls, f).offset, (name, f)
 
 
 def test_strerror_and_version(lib):

@@ -416,3 +416,43 @@ def test_fe_row_slabs_are_rows_of_the_full_matrix():
         assert np.array_equal(S.rowptr, A.rowptr[lo:hi + 1] - a)
         assert np.array_equal(S.col, A.col[a:b])
         assert np.array_equal(S.val.view(np.int64), A.val[a:b].view(np.int64))
+
+
+# ------------------------------------------------------------------ bounded communication
+def test_bounded_setup_large_k_equals_full():
+    """k >= n_p: every lower stripe is gathered, so each stripe's rows equal the
+    whole-matrix set-up (row independence)."""
+    A = ai.poisson3d(10)
+    bounds = [0, 250, 500, 750, 1000]
+    G = oracle.setup(A, 20, 2)
+    for p in range(4):
+        res, used = oracle.setup_bounded(A, bounds, p, 4, 20, 2)
+        assert used == list(range(p + 1))
+        for t, i in enumerate(range(bounds[p], bounds[p + 1])):
+            c0, v0 = G.row(i)
+            c1, v1 = res.row(t)
+            assert np.array_equal(c0, c1) and np.array_equal(v0.view(np.int64), v1.view(np.int64))
+
+
+def test_bounded_setup_k1_truncates():
+    """Stripes of 2 planes and k = 1 on a 7-point grid: A-hat is tridiagonal, stripe p
+    sees only p-1 and p; patterns stay inside I_p, rows near the lower boundary of
+    I_p lose entries, and the local optimality (Eq. 7) holds on A[I_p, I_p]."""
+    nx = 10
+    A = ai.poisson3d(nx)
+    bounds = [q * 2 * nx * nx for q in range(6)]
+    H = oracle.comm_matrix(A, bounds)
+    assert np.array_equal(H, np.eye(5, dtype=bool) | np.eye(5, k=1, dtype=bool) | np.eye(5, k=-1, dtype=bool))
+    full = oracle.setup(A, 20, 2)
+    res, used = oracle.setup_bounded(A, bounds, 3, 1, 20, 2)
+    assert used == [2, 3]
+    lo = bounds[2]
+    differ = 0
+    for t, i in enumerate(range(bounds[3], bounds[4])):
+        c, v = res.row(t)
+        assert c.min() >= lo
+        c0, _ = full.row(i)
+        differ += not np.array_equal(c, c0)
+    assert differ > 0
+    # rows near the top of the stripe reach at most 20 hops ~ 2 planes: some may still match
+    assert res.reason.max() <= 2
