@@ -760,7 +760,7 @@ static int dist_apply_ext(afsai_ctx_t ctx, afsai_factor_t F, double *re, double 
     if (pw) a.st = pw->state.as<PcgState>();
     {
         KTimer kt(ctx, AFSAI_K_SPMV_G);
-        launch_spmv(a, 0, spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1)), grid, st);
+        launch_spmv(a, 0, spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1), 1), grid, st);
     }
     {
         KTimer kt(ctx, AFSAI_K_COMM);
@@ -779,7 +779,7 @@ static int dist_apply_ext(afsai_ctx_t ctx, afsai_factor_t F, double *re, double 
     }
     {
         KTimer kt(ctx, AFSAI_K_SPMV_GT);
-        launch_spmv(c, mode, spmv_group_width((double)F->nnz_Gt / std::max<int64_t>(n, 1)), grid, st);
+        launch_spmv(c, mode, spmv_group_width((double)F->nnz_Gt / std::max<int64_t>(n, 1), 2), grid, st);
     }
     ctx->launches += 2;
     AFSAI_CUDA_TRY(cudaGetLastError());
@@ -855,7 +855,7 @@ int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const do
     const int64_t *arp = A.rowptr;
     const int32_t *aci = A.col - A.base;
     const double *av = A.val - A.base;
-    const int wA = spmv_group_width((double)A.nnz / std::max<int64_t>(n, 1));
+    const int wA = spmv_group_width((double)A.nnz / std::max<int64_t>(n, 1), 0);
     auto allreduce = [&](int k) -> int {
         KTimer kt(ctx, AFSAI_K_COMM);
         AFSAI_NCCL_TRY(ncclAllReduce(&S->sum[k], &S->sum[k], 1, ncclDouble, ncclSum, ctx->comm, st));

@@ -880,7 +880,7 @@ void launch_apply_local(afsai_ctx_t ctx, afsai_factor_t F, const double *r, doub
     if (pw) a.st = pw->state.as<PcgState>();
     {
         KTimer kt(ctx, AFSAI_K_SPMV_G);
-        launch_spmv(a, 0, spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1)), grid, ctx->stream);
+        launch_spmv(a, 0, spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1), 1), grid, ctx->stream);
     }
     SpmvArgs b = spmv_args(n, F->t_rowptr.as<int64_t>(), F->t_col.as<int32_t>(), F->t_val.as<double>(), t, 0, z);
     if (pw) {
@@ -891,7 +891,7 @@ void launch_apply_local(afsai_ctx_t ctx, afsai_factor_t F, const double *r, doub
     }
     {
         KTimer kt(ctx, AFSAI_K_SPMV_GT);
-        launch_spmv(b, mode, spmv_group_width((double)F->nnz_Gt / std::max<int64_t>(n, 1)), grid, ctx->stream);
+        launch_spmv(b, mode, spmv_group_width((double)F->nnz_Gt / std::max<int64_t>(n, 1), 2), grid, ctx->stream);
     }
     ctx->launches += 2;
 }
@@ -985,7 +985,7 @@ int local_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const d
     const int64_t *arp = A.rowptr;
     const int32_t *aci = A.col - A.base;
     const double *av = A.val - A.base;
-    const int wA = spmv_group_width((double)A.nnz / std::max<int64_t>(n, 1));
+    const int wA = spmv_group_width((double)A.nnz / std::max<int64_t>(n, 1), 0);
 
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[5], st));
     {

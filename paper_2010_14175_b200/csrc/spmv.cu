@@ -132,25 +132,34 @@ static void launch_w(const SpmvArgs &a, int mode, int grid, cudaStream_t st) {
     }
 }
 
-int spmv_group_width(double avg_nnz) {
-    // miniwarp size chosen from the mean row length, 4..32;
-    // AFSAI_SPMV_WIDTH overrides (experiments)
-    static int forced = -1;
-    if (forced < 0) {
+int spmv_group_width(double avg_nnz, int which) {
+    // miniwarp size chosen from the mean row length, 1..32;
+    // AFSAI_SPMV_WIDTH (all) or AFSAI_SPMV_WIDTH_A / _G / _GT override (experiments)
+    static const char *names[3] = {"AFSAI_SPMV_WIDTH_A", "AFSAI_SPMV_WIDTH_G", "AFSAI_SPMV_WIDTH_GT"};
+    static int forced[4] = {-1, -1, -1, -1};
+    if (forced[3] < 0) {
         const char *e = std::getenv("AFSAI_SPMV_WIDTH");
-        forced = e ? std::atoi(e) : 0;
+        forced[3] = e ? std::atoi(e) : 0;
+        for (int k = 0; k < 3; ++k) {
+            const char *f = std::getenv(names[k]);
+            forced[k] = f ? std::atoi(f) : forced[3];
+        }
     }
-    if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
-    // measured on B200 (scripts/spmv_sweep.py, M2): 8 lanes for ~41 nnz/row reach
-    // 5.0 TB/s vs 2.5 TB/s with 32 -- more rows in flight beats lane utilisation
-    if (avg_nnz < 16) return 4;
-    if (avg_nnz < 96) return 8;
+    const int fw = forced[which < 0 || which > 2 ? 0 : which];
+    if (fw == 1 || fw == 2 || fw == 4 || fw == 8 || fw == 16 || fw == 32) return fw;
+    // measured on B200 (scripts/pcg_kernel_times.py, profiles/r02_spmv_width_M3.jsonl):
+    // short rows want few lanes per row (more rows, hence more loads, in flight)
+    if (avg_nnz < 12) return 1;
+    if (avg_nnz < 24) return 2;
+    if (avg_nnz < 96) return 4;
     if (avg_nnz < 256) return 16;
     return 32;
 }
 
 void launch_spmv(const SpmvArgs &a, int mode, int width, int grid, cudaStream_t st) {
     switch (width) {
+        case 1: launch_w<1>(a, mode, grid, st); break;
+        case 2: launch_w<2>(a, mode, grid, st); break;
         case 4: launch_w<4>(a, mode, grid, st); break;
         case 8: launch_w<8>(a, mode, grid, st); break;
         case 16: launch_w<16>(a, mode, grid, st); break;

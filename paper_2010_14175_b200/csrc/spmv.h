@@ -29,7 +29,8 @@ struct SpmvArgs {
     int sum_idx;             // mode 4: local dot stored in st->sum[sum_idx]
 };
 
-int spmv_group_width(double avg_nnz);
+// which: 0 = A, 1 = G, 2 = G^T (per-operand override of the miniwarp width)
+int spmv_group_width(double avg_nnz, int which);
 // mode 0: y = M x; 1: + dot(y, w) -> alpha; 2: + dot(y, w) -> beta, rz; 3: + dot(y, w) -> rz
 void launch_spmv(const SpmvArgs &a, int mode, int width, int grid, cudaStream_t st);
 void launch_pcg_init(int64_t n, const double *b, double *x, double *r, double *partials, unsigned *counter,
