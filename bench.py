@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--workload", default="M3", choices=["M2", "M3", "M4", "M5"])
     ap.add_argument("--weak", action="store_true", help="round-1 weak scaling: a 100^3 Poisson slab per GPU")
     ap.add_argument("--e2e-runs", type=int, default=5)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="set-up arithmetic (fp32: PAPER.md P:953-965; apply/PCG stay fp64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -257,7 +259,7 @@ def main():
             torch.distributed.barrier()
 
     def step():
-        F = Factor(ctx, dA, NSTEPS, S, EPS, CAP)
+        F = Factor(ctx, dA, NSTEPS, S, EPS, CAP, precision=args.precision)
         _, rep = F.pcg(b, tol=TOL, max_iters=20000, x=x)
         return F, rep
 
@@ -324,6 +326,8 @@ def main():
     # fp64 ALU peak from unit counts and clock: 148 SM x 64 DFMA/clk x 2 flop
     nsm = torch.cuda.get_device_properties(local).multi_processor_count
     fp64_peak_tf = nsm * 64 * 2 * sm_max * 1e6 / 1e12
+    if args.precision == "fp32":   # the fp32 set-up runs on the FFMA pipe: 128 FMA/clk/SM
+        fp64_peak_tf = nsm * 128 * 2 * sm_max * 1e6 / 1e12
     setup_flop = 2.0 * (stats["fma_border"] + stats["fma_backsub"] + stats["fma_grad"])
     dfma_probe_tf = ctx.dfma_peak()[0] / 1e12
     per_class = {k: {"launches": v[0] // args.steps, "ms_per_step": v[1] / args.steps} for k, v in ktimes.items()}
@@ -343,7 +347,9 @@ def main():
                 "bound": "alu", "achieved": achieved,
                 "peak": fp64_peak_tf, "unit": "TFLOP/s", "frac": achieved / fp64_peak_tf, "traffic": traffic,
                 "traffic_unit": f"bytes per launch (dram read + write, ncu --set full, profiles/{tfile})",
-                "peak_source": (f"{nsm} SM x 64 DFMA/clk x 2 x {sm_max:.0f} MHz (unit counts, B200_PROFILING.md; "
+                "peak_source": (f"{nsm} SM x {64 if args.precision == 'fp64' else 128} "
+                                f"{'DFMA' if args.precision == 'fp64' else 'FFMA'}/clk x 2 x {sm_max:.0f} MHz "
+                                f"(unit counts, B200_PROFILING.md; "
                                 f"MEASURED_PEAKS.json has no fp64 entry); in-run DFMA probe "
                                 f"{dfma_probe_tf:.1f} TF/s (afsai_probe_dfma_peak)"),
                 "algorithmic_flop_per_launch": setup_flop, "avg_launch_ms": setup_ms}
@@ -395,7 +401,7 @@ def main():
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
-            F = Factor(ctx, hA, NSTEPS, S, EPS, CAP)
+            F = Factor(ctx, hA, NSTEPS, S, EPS, CAP, precision=args.precision)
             F.pcg(hb, tol=TOL, max_iters=20000, x=hx)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
@@ -421,12 +427,14 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
                 "scaling": "weak" if args.weak else "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32 set-up, f64 solve",
+                "data": "synthetic",
                 "config": {"workload": (f"M2 weak scaling: 3D 7-point Poisson {nx}^3 per GPU (global "
                                         f"{nx}x{nx}x{nx * world}), aFSAI {NSTEPS}x{S}, PCG to {TOL}") if args.weak
                            else f"{wname}: {ai.CONFIGS[wname]['desc']}, PCG to {TOL}, rows split over {world} GPU(s)",
                            "global_rows": Aglob.n, "nnz_A": Aglob.nnz, "nsteps": NSTEPS, "s": S, "eps": EPS,
                            "max_row_nnz": CAP, "pcg_tol": TOL, "parallelism": f"rows{world}",
+                           "setup_precision": args.precision,
                            "l2": "flushed (256 MiB write) between timed steps; A+G+scratch > 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks, **extra}

@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, varia
     lib_out = LIB_DBG if debug else LIB
     extra = ["-DAFSAI_BOUNDS_CHECK"] if debug else []
     if variant:
-        objdir = os.path.join(HERE, "build_obj_" + variant)
+        objdir = os.path.join("/tmp", "afsai_build_obj_" + variant)  # outside the repo (gpurun snapshot size)
         lib_out = os.path.join(LIBDIR, f"libafsai_b200_{variant}.so")
         extra = extra + ["-D" + d for d in defines]
     os.makedirs(LIBDIR, exist_ok=True)

@@ -189,7 +189,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         const int l = std::atoi(e);
         if (l == 32 || (l == 16 && mmax <= 96)) lpr = l;
     }
-    bool hits = max_row_len <= 9;  // one entry per lane at 16 lanes per row
+    // one entry per lane at 16 lanes per row; hits may record int32 entry indices
+    bool hits = max_row_len <= 9 && Aext.nnz < INT32_MAX;
     if (const char *e = std::getenv("AFSAI_HITS")) hits = hits && std::atoi(e) != 0;
     // lockstep: ls_lpr lanes per row, 32/ls_lpr rows per warp (rows <= ls_lpr entries, s <= 4)
     int ls_lpr = 16;

@@ -114,8 +114,17 @@ __device__ __forceinline__ int hinsert(int32_t *hkey, int H, int log2H, int32_t 
 __device__ __forceinline__ int tri(int q) { return (q * (q + 1)) >> 1; }
 
 // (|a|, ja) better than (|b|, jb)?  |acc| descending, then column ascending.
-__device__ __forceinline__ bool better(real aa, int32_t ja, real ab, int32_t jb) {
-    return (aa > ab) || (aa == ab && ja < jb);
+// The magnitudes are |acc| >= 0 or the sentinel -1: for non-negative IEEE values
+// the order of the bit patterns (as signed integers) is the numeric order, and the
+// sentinel's sign bit makes it smaller than all of them, so the comparison runs on
+// the integer pipe (same result as the floating-point compare).
+__device__ __forceinline__ bool better(double aa, int32_t ja, double ab, int32_t jb) {
+    const long long ia = __double_as_longlong(aa), ib = __double_as_longlong(ab);
+    return (ia > ib) || (ia == ib && ja < jb);
+}
+__device__ __forceinline__ bool better(float aa, int32_t ja, float ab, int32_t jb) {
+    const int ia = __float_as_int(aa), ib = __float_as_int(ab);
+    return (ia > ib) || (ia == ib && ja < jb);
 }
 
 __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {

@@ -22,7 +22,7 @@ namespace AFSAI_PNS {
 // through a group-aggregated allocation (free stack first, then high-water).
 template <int LPR, int HC>
 __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int log2H, int32_t i, bool valid,
-                              int32_t c, real v, int q, real *arow_u, real *brow_u) {
+                              int32_t c, real v, int32_t e, int q, real *arow_u, real *brow_u) {
     const int CA = w.CA;
     const int32_t r = q < 0 ? i : w.P[q];
     bool need = false;
@@ -41,7 +41,7 @@ __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int
                 if (st >= 0) {
                     if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
                 } else if (st <= -2) {
-                    hit_insert<HC>(w, -2 - st, q, r, v);     // existing candidate: new hit
+                    hit_insert<HC>(w, -2 - st, q, r, AFSAI_HIT(v, e));  // existing candidate: new hit
                 }                                            // st == -1: dropped (row overflowed)
             }
         }
@@ -63,7 +63,7 @@ __device__ void scan_row_hits(const HitState &w, const Group<LPR> &G, int H, int
                 w.ahs[aa] = (int16_t)sl;
                 w.ahn[aa] = 1;
                 w.ahq[aa] = (int8_t)q;
-                w.hv[aa] = v;
+                w.hv[aa] = AFSAI_HIT(v, e);
             }
             atomicAdd(&w.misc[0], 1);
         }
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             const bool vi = gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
             const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
-            scan_row_hits<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr);
+            scan_row_hits<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, (int32_t)(e0i + gl), -1, nullptr, nullptr);
         }
         const real a_ii = w.dscr[0];
         const real psi0 = a_ii;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                     if (h < n) {
                         const int q = w.ahq[h * CA + aa];
                         const real gv = q < 0 ? real(1) : w.g[q];
-                        acc = fma(w.hv[h * CA + aa], gv, acc);
+                        acc = fma(AFSAI_HITVAL(a, w.hv[h * CA + aa]), gv, acc);
                     }
                 }
                 c_gfma += n;
@@ -249,19 +249,20 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             PHASE(2)
             // ---- phase A: gather the new rows (one row per pass), record hits
             for (int ug = 0; ug < nsel; ug += GS) {
-                int32_t pc[GS];
+                int32_t pc[GS], pe[GS];
                 real pv[GS];
                 bool pvld[GS];
 #pragma unroll
                 for (int u = 0; u < GS; ++u) {  // every row's entries in flight at once
                     pvld[u] = (ug + u < nsel) && gl < w.glen[ug + u];
+                    pe[u] = (int32_t)(w.gstart[ug + u] + gl);
                     pc[u] = pvld[u] ? __ldg(a.col + w.gstart[ug + u] + gl) : 0;
                     pv[u] = pvld[u] ? __ldg(aval(a) + w.gstart[ug + u] + gl) : real(0);
                 }
 #pragma unroll
                 for (int u = 0; u < GS; ++u)
                     if (ug + u < nsel)
-                        scan_row_hits<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + ug + u,
+                        scan_row_hits<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], pe[u], m + ug + u,
                                                w.arow + (ug + u) * w.M, w.brow + ug + u);
             }
             PHASE(3)

@@ -6,8 +6,17 @@
 namespace afsai {
 namespace AFSAI_PNS {
 
+// A recorded hit (candidate j, pattern row r) is the int32 index of the entry
+// (r, j) in A's arrays, not the value a_jr: 4 bytes instead of 8 per hit, so more
+// rows fit in shared memory (M3: 14 -> 16 rows per SM); the gradient re-reads the
+// value (an L1/L2 hit, the same bits).  Needs nnz(A_ext) < 2^31 (run_rows).
+typedef int32_t hit_t;
+#define AFSAI_HIT(v, e) (e)
+#define AFSAI_HITVAL(a, h) __ldg(aval(a) + (h))
+
 struct HitState {
-    real *inv, *y, *g, *L, *arow, *brow, *dscr, *hv, *acc;
+    real *inv, *y, *g, *L, *arow, *brow, *dscr, *acc;
+    hit_t *hv;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey;
     int16_t *ahs, *afree;
@@ -17,10 +26,9 @@ struct HitState {
 
 template <int HC>
 __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc) {
-    int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (int64_t)CA * HC +
-                  (acc ? CA : 0);
+    int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (acc ? CA : 0);
     int64_t i64 = S;
-    int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA;
+    int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA + (int64_t)CA * HC;  // ... akey, hv
     int64_t i16 = 2 * (int64_t)CA;
     int64_t i8 = (int64_t)H + CA + (int64_t)CA * HC;
     int64_t b = real_bytes(dbl) + i64 * 8 + i32 * 4 + i16 * 2 + i8;
@@ -43,7 +51,6 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.arow = d; d += S * M;
     w.brow = d; d += S;
     w.dscr = d; d += 2;
-    w.hv = d; d += CA * HC;  // [h][a]
     w.acc = nullptr;
     if (acc) { w.acc = d; d += CA; }
     int64_t *l8 = reinterpret_cast<int64_t *>(base + real_bytes(d - reinterpret_cast<real *>(base)));
@@ -56,6 +63,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.glen = ip; ip += S;
     w.misc = ip; ip += 8;
     w.akey = ip; ip += CA;
+    w.hv = ip; ip += CA * HC;  // [h][a]
     int16_t *sp = reinterpret_cast<int16_t *>(ip);
     w.ahs = sp; sp += CA;
     w.afree = sp; sp += CA;
@@ -71,7 +79,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
 // Insert the hit (column r at pattern position q, value v) into active slot aa,
 // keeping the list sorted by r; q = -1 stands for r = i (always last).
 template <int HC>
-__device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int32_t r, real v) {
+__device__ __forceinline__ void hit_insert(const HitState &w, int aa, int q, int32_t r, hit_t v) {
     const int CA = w.CA;
     int n = w.ahn[aa];
     if (n >= HC) {

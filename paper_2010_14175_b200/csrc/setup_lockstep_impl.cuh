@@ -59,7 +59,7 @@ struct RowBook {
 
 // hit_insert of setup_hits.cuh; returns false when the list is full
 template <int HC>
-__device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, int32_t r, real v) {
+__device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, int32_t r, hit_t v) {
     const int CA = w.CA;
     const int n = w.ahn[aa];
     if (n >= HC) return false;
@@ -86,7 +86,7 @@ __device__ __forceinline__ bool hit_insert_ls(const HitState &w, int aa, int q, 
 // tables to the next call.
 template <int LPR, int HC>
 __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H, int log2H, int32_t i, bool valid,
-                                 int32_t c, real v, int q, real *arow_u, real *brow_u, RowBook &b) {
+                                 int32_t c, real v, int32_t e, int q, real *arow_u, real *brow_u, RowBook &b) {
     const int CA = w.CA;
     bool need = false;
     int sl = -1;
@@ -105,7 +105,7 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
                     if (q >= 0 && st <= q) arow_u[st] = v;  // gather A[P_q, P_st]
                 } else if (st <= -2) {                      // existing candidate: new hit
                     const int32_t r = q < 0 ? i : w.P[q < w.M ? q : 0];
-                    if (!hit_insert_ls<HC>(w, -2 - st, q, r, v)) { b.ovf = true; b.why |= 4u; }
+                    if (!hit_insert_ls<HC>(w, -2 - st, q, r, AFSAI_HIT(v, e))) { b.ovf = true; b.why |= 4u; }
                 }                                            // st == -1: dropped (row overflowed)
             }
         }
@@ -124,7 +124,7 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
             w.ahs[aa] = (int16_t)sl;
             w.ahn[aa] = 1;
             w.ahq[aa] = (int8_t)q;
-            w.hv[aa] = v;
+            w.hv[aa] = AFSAI_HIT(v, e);
         }
     }
     const int k = __popc(bal);
@@ -208,11 +208,14 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
             real l[GS];
-#pragma unroll
-            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
+            // the owner stores L[q][k] (a predicated store, no divergence) and every
+            // lane reads it back: a shared-memory broadcast instead of 64-bit shuffles
 #pragma unroll
             for (int u = 0; u < GS; ++u)
-                if (live && st[u]) Lnew[u][k] = l[u];  // every lane of the row stores the same bits
+                if (gl == ln && live && st[u]) Lnew[u][k] = t[u][tt] * ivc[tt];
+            G.sync();
+#pragma unroll
+            for (int u = 0; u < GS; ++u) l[u] = Lnew[u][k];  // dead rows: any value, folded into dead state
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
@@ -300,8 +303,9 @@ __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];  // L[k][c]; c >= k: dead
             pk -= k;
-            const real gk = G.bcast(tb[tt] * ivc[tt], ln);
-            if (live) w.g[k] = gk;  // broadcast value, stored by every lane of the row
+            if (gl == ln && live) w.g[k] = tb[tt] * ivc[tt];
+            G.sync();
+            const real gk = w.g[k];
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) fma_if(live, -lk[t2], gk, tb[t2]);
         }
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             const bool vi = has && gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
             const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
-            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, -1, nullptr, nullptr, bk);
+            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, (int32_t)(e0i + gl), -1, nullptr, nullptr, bk);
         }
         const real a_ii = w.dscr[0];
         const real psi0 = a_ii;
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                         if (h < n) {
                             const int q = w.ahq[h * CA + aa];
                             const real gv = q < 0 ? real(1) : w.g[q];
-                            acc = fma(w.hv[h * CA + aa], gv, acc);
+                            acc = fma(AFSAI_HITVAL(a, w.hv[h * CA + aa]), gv, acc);
                         }
                     }
                     c_gfma += n;
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             //      heads; every lane keeps the winners (selj) and their ranks in
             //      registers, the winner's lane stores its slot and row extent
             int32_t selj[GS];
-            int32_t pc[GS];
+            int32_t pc[GS], pe[GS];
             real pv[GS];
             bool pvld[GS];
 #pragma unroll
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     const int gn = G.bcast((int)(re[0] - rs[0]), wl);
                     pvld[u] = (u < nsel) && gl < gn;
                     pc[u] = pvld[u] ? __ldg(a.col + g0 + gl) : 0;
+                    pe[u] = (int32_t)(g0 + gl);
                     pv[u] = pvld[u] ? __ldg(aval(a) + g0 + gl) : real(0);
                     if (won) {
                         w.sela[u] = bt[0];
@@ -485,9 +490,13 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
 #pragma unroll
                 for (int v = 0; v < GS; ++v) rk[u] += (selj[v] < selj[u]);
             }
+            // what border reads: the whole of each new row's gather slot, by fixed
+            // per-lane column tiles (predicated stores, no row-dependent loop)
 #pragma unroll
             for (int u = 0; u < GS; ++u)
-                for (int c = gl; c < m + nsel; c += LPR) w.arow[u * w.M + c] = real(0);  // what border reads
+#pragma unroll
+                for (int tt = 0; tt < NT; ++tt)
+                    if (gl + LPR * tt < w.M) w.arow[u * w.M + gl + LPR * tt] = real(0);
             if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             if (gl < nsel) {
@@ -511,7 +520,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                 for (int u = 0; u < GS; ++u)
                     if (ug + u < nsel_max) {  // winner u (selection order) is pattern position m + rk[u]
                         const int r = rk[u] < GS ? rk[u] : 0;
-                        scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], m + r,
+                        scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], pe[u], m + r,
                                                   w.arow + r * w.M, w.brow + r, bk);
                     }
             }

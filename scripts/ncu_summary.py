@@ -13,9 +13,19 @@ KEEP = {"Duration", "SM Frequency", "Elapsed Cycles", "Compute (SM) Throughput",
         "Achieved Active Warps Per SM", "Theoretical Occupancy", "Active Warps Per Scheduler",
         "Eligible Warps Per Scheduler", "Warp Cycles Per Issued Instruction", "Avg. Active Threads Per Warp",
         "Avg. Not Predicated Off Threads Per Warp"}
+# NCU_ID=<launch id> picks one launch of a multi-launch capture (default: the longest)
+import os
 det = list(csv.reader(open(sys.argv[1])))
 hdr = det[0]
 ix = {h: i for i, h in enumerate(hdr)}
+_dur = {}
+for r in det[1:]:
+    if r[ix["Metric Name"]] == "Duration":
+        f = float(r[ix["Metric Value"]].replace(",", ""))
+        _dur[r[ix["ID"]]] = f * {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}.get(r[ix["Metric Unit"]], 1.0)
+pick = os.environ.get("NCU_ID") or (max(_dur, key=_dur.get) if _dur else "0")
+det = [det[0]] + [r for r in det[1:] if r[ix["ID"]] == pick]
+print(f"launch id {pick} of {len(_dur)} captured")
 kname = det[1][ix["Kernel Name"]] if "Kernel Name" in ix else "?"
 print(f"kernel: {kname}")
 seen = set()
@@ -25,7 +35,8 @@ for r in det[1:]:
         seen.add(n)
         print(f"  {n:45s} {r[ix['Metric Value']]:>16s} {r[ix['Metric Unit']]}")
 raw = list(csv.reader(open(sys.argv[2])))
-h, v = raw[0], raw[2]
+h = raw[0]
+v = next(r for r in raw[2:] if r[h.index("ID")] == pick)
 items = [(a, b) for a, b in zip(h, v) if "pcsamp_warps_issue_stalled" in a and not a.endswith("not_issued")]
 tot = sum(float(b.replace(",", "") or 0) for _, b in items)
 print("stall reasons (share of PC samples):")

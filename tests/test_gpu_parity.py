@@ -79,9 +79,16 @@ CASES = [
     ("fe_4_10x2_cap15", lambda: ai.fe_elasticity(4), 10, 2, 0.0, 15),
     ("rsparse_s4", lambda: ai.random_sparse_spd(3000, 10, sub=6), 8, 4, 0.0, 1 << 30),
     ("hetero_32_probe", lambda: ai.hetero_poisson3d(32), 20, 2, 0.0, 1 << 30),
+    # s > 4 on a stencil: the hit-list kernel that is not in lockstep
+    ("poisson3d_8_s5", lambda: ai.poisson3d(8), 4, 5, 0.0, 1 << 30),
     # hub column: G^T row 0 is ~n long (the long-row transpose sort, > 1024 entries)
     ("arrow_3000_12x3", lambda: ai.arrow_spd(3000), 12, 3, 0.0, 1 << 30),
 ]
+
+
+# the kernel plan each case must exercise (afsai_setup_stats_t.plan)
+PLAN = {"M1_poisson2d_32": 0, "poisson3d_12_20x2": 0, "hetero_10_20x2": 0, "fe_5_30x3_cap100": 1,
+        "rsparse_cap12_s5": 3, "poisson3d_8_s5": 2, "fe_4_12x1": 1}
 
 
 @pytest.mark.parametrize("name,make,k,s,eps,cap", CASES, ids=[c[0] for c in CASES])
@@ -100,6 +107,8 @@ def test_setup_parity(ctx, name, make, k, s, eps, cap):
     assert np.array_equal(st.cpu().numpy(), ref.steps)
     assert np.array_equal(rs.cpu().numpy(), ref.reason)
     stats = F.stats()
+    if name in PLAN:
+        assert stats["plan"] == PLAN[name], (name, stats["plan"])
     assert stats["nnz_G"] == Gr.nnz
     assert sum(stats["rows_by_reason"]) == A.n
     # transpose: exact, rows ascending (C10)
