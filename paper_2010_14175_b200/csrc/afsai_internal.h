@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -149,6 +150,15 @@ struct afsai_ctx_s {
 };
 
 namespace afsai {
+// NVTX range of one phase of a call (header-only NVTX v3: a no-op unless a tool
+// such as Nsight Systems is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 // RAII: events around the launches of one kernel class when timing is enabled
 struct KTimer {
     afsai_ctx_t c;

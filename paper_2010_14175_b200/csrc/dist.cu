@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "assemble.h"
@@ -62,6 +64,27 @@ static RangePlan make_range_plan(int me, int nranks, const std::vector<int64_t> 
         if (r1 > r0) P.recvs.push_back({q, r0, r1 - r0});
     }
     return P;
+}
+
+// Wait for the context stream while polling NCCL's asynchronous error state: a
+// failed or vanished peer would otherwise leave cudaStreamSynchronize waiting
+// forever inside a collective.  On an NCCL error the communicator is aborted
+// (the context then refuses further collective calls) and AFSAI_ENCCL returned.
+static int sync_poll(afsai_ctx_t ctx, afsai_status_t *status) {
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(ctx->stream);
+        if (e == cudaSuccess) return AFSAI_OK;
+        if (e != cudaErrorNotReady)
+            return set_status(status, AFSAI_ECUDA, std::string("stream error: ") + cudaGetErrorString(e));
+        ncclResult_t r = ncclSuccess;
+        if (ctx->comm && ncclCommGetAsyncError(ctx->comm, &r) == ncclSuccess && r != ncclSuccess &&
+            r != ncclInProgress) {
+            ncclCommAbort(ctx->comm);
+            ctx->comm = nullptr;
+            return set_status(status, AFSAI_ENCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+        }
+        std::this_thread::yield();
+    }
 }
 
 // exchange a RangePlan on an extended buffer ext (index = global - lo) of `elem` bytes
@@ -209,6 +232,7 @@ int block_rows_to_G(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_
 // extended CSR of rows [lo, e).
 static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<int64_t> &bounds, int64_t lo,
                        DeviceCsr *X, afsai_status_t *status) {
+    NvtxRange nv("afsai set-up halo exchange");
     cudaStream_t st = ctx->stream;
     const int me = ctx->rank, np = ctx->nranks;
     const int64_t b = bounds[me], e = bounds[me + 1];
@@ -314,6 +338,7 @@ struct DbgTimer {
 
 static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<int64_t> &bounds,
                           afsai_status_t *status) {
+    NvtxRange nv("afsai G^T exchange + transpose");
     cudaStream_t st = ctx->stream;
     DbgTimer dt(st);
     dt.mark("start");
@@ -558,6 +583,7 @@ static int truncate_to_stripes(afsai_ctx_t ctx, const DeviceCsr &X, const std::v
 
 int dist_setup(afsai_ctx_t ctx, const afsai_csr_t *Ain, const afsai_params_t *p, afsai_factor_t *out,
                afsai_status_t *status) {
+    if (!ctx->comm) return set_status(status, AFSAI_ENCCL, "the context's communicator was aborted");
     cudaStream_t st = ctx->stream;
     DeviceCsr A;
     int rc = agree(ctx, stage_csr(ctx, Ain, &A, status), status);
@@ -787,6 +813,7 @@ static int dist_apply_ext(afsai_ctx_t ctx, afsai_factor_t F, double *re, double 
 }
 
 int dist_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z, afsai_status_t *status) {
+    if (!ctx->comm) return set_status(status, AFSAI_ENCCL, "the context's communicator was aborted");
     if (!F->dist) return set_status(status, AFSAI_EINVAL, "factor was not built on this communicator");
     DistState *D = dstate(F);
     cudaStream_t st = ctx->stream;
@@ -816,6 +843,7 @@ int dist_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z, af
 // r.z together (two all-reduces per iteration).
 int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const double *b_in, double *x, double tol,
              int32_t max_iters, afsai_pcg_report_t *rep, afsai_status_t *status) {
+    if (!ctx->comm) return set_status(status, AFSAI_ENCCL, "the context's communicator was aborted");
     if (!F->dist) return set_status(status, AFSAI_EINVAL, "factor was not built on this communicator");
     DistState *D = dstate(F);
     cudaStream_t st = ctx->stream;
@@ -920,7 +948,7 @@ int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const do
         }
         AFSAI_CUDA_TRY(cudaGetLastError());
         AFSAI_CUDA_TRY(cudaMemcpyAsync(&hs, S, sizeof hs, cudaMemcpyDeviceToHost, st));
-        AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+        if ((rc = sync_poll(ctx, status))) return rc;
         if (hs.done || it >= max_iters) break;
     }
     AFSAI_CUDA_TRY(cudaEventRecord(ctx->ev[6], st));
@@ -939,7 +967,7 @@ int dist_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const do
     if ((rc = allreduce(3))) return rc;
     AFSAI_CUDA_TRY(cudaMemcpyAsync(&hs, S, sizeof hs, cudaMemcpyDeviceToHost, st));
     if (!xdev) AFSAI_CUDA_TRY(cudaMemcpyAsync(x, xd, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+    if ((rc = sync_poll(ctx, status))) return rc;
     const bool conv = hs.done == 1 || hs.bnorm2 == 0.0;
     if (rep) {
         rep->iters = hs.iters;

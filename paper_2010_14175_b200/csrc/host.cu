@@ -98,6 +98,7 @@ static float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 // Validate A (a0): structure, diagonal, finiteness; returns max row length.
 int validate_csr(afsai_ctx_t ctx, const DeviceCsr &A, int64_t *max_row_len, afsai_status_t *status) {
+    NvtxRange nv("afsai validate A");
     DevBuf err;
     AFSAI_CUDA_TRY(err.alloc(2 * sizeof(unsigned long long), ctx->stream));
     AFSAI_CUDA_TRY(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -152,6 +153,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     // The candidate table starts small (stencil universes are small); rows that
     // overflow an on-chip table are retried with 4x larger tables.
     // AFSAI_LPR / AFSAI_TABLE / AFSAI_HITS=0 override (experiments).
+    NvtxRange nv("afsai set-up rows kernel");
     // the kernel instances of the set-up precision (afsai::dp fp64, afsai::sp fp32)
     const bool f32 = p.precision == AFSAI_PREC_FP32;
     auto scan_kernel_for = f32 ? sp::scan_kernel_for : dp::scan_kernel_for;
@@ -649,6 +651,7 @@ int afsai_ctx_kernel_times(afsai_ctx_t ctx, int64_t launches[AFSAI_K_NCLASSES], 
 
 int afsai_setup(afsai_ctx_t ctx, const afsai_csr_t *A, const afsai_params_t *p, afsai_factor_t *out,
                 afsai_status_t *status) {
+    NvtxRange nv("afsai_setup");
     set_status(status, AFSAI_OK, "");
     if (!ctx || !A || !p || !out) return set_status(status, AFSAI_EINVAL, "null argument");
     if (A->n_rows < 0 || A->n_cols < 1 || A->nnz < 0 || A->row_begin < 0 || A->row_begin + A->n_rows > A->n_cols ||
@@ -787,6 +790,7 @@ int SetupWork::read_stats(afsai_ctx_t ctx, afsai_setup_stats_t *s, afsai_status_
 
 // count -> scan -> fill (a7).  The scratch rows are already sorted by column.
 int assemble_G(afsai_ctx_t ctx, afsai_factor_t F, SetupWork &W, int64_t n, int32_t stride, afsai_status_t *status) {
+    NvtxRange nv("afsai assemble G");
     cudaStream_t st = ctx->stream;
     DevBuf tiles;
     AFSAI_CUDA_TRY(tiles.alloc(scan_tmp_elems(n) * sizeof(int64_t) + 16, st));
@@ -812,6 +816,7 @@ int assemble_G(afsai_ctx_t ctx, afsai_factor_t F, SetupWork &W, int64_t n, int32
 // G^T of the local G (1 GPU: col_lo = 0, n_out = n): count columns, scan,
 // scatter, then sort each row by source row (C10).
 int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out, afsai_status_t *status) {
+    NvtxRange nv("afsai transpose G");
     cudaStream_t st = ctx->stream;
     DevBuf cnt, tiles, tcol, tval;
     const int64_t nnz = F->nnz_G;
@@ -902,6 +907,7 @@ void launch_apply_local(afsai_ctx_t ctx, afsai_factor_t F, const double *r, doub
 extern "C" {
 
 int afsai_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z) {
+    NvtxRange nv("afsai_apply");
     afsai_status_t *status = nullptr;
     if (!ctx || !F || !r || !z || r == z) return AFSAI_EINVAL;
     if (F->ctx != ctx || F->block) return AFSAI_EINVAL;  // another context's factor / a block factor (no G^T)
@@ -933,6 +939,7 @@ int afsai_apply(afsai_ctx_t ctx, afsai_factor_t F, const double *r, double *z) {
 
 int afsai_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const double *b, double *x, double tol,
               int32_t max_iters, afsai_pcg_report_t *rep, afsai_status_t *status) {
+    NvtxRange nv("afsai_pcg");
     set_status(status, AFSAI_OK, "");
     if (!ctx || !Ain || !F || !b || !x || !(tol > 0.0) || max_iters < 1)
         return set_status(status, AFSAI_EINVAL, "bad PCG arguments");

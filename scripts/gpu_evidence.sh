@@ -22,15 +22,18 @@ if [ -z "$SKIP_BENCH" ]; then
 fi
 if [ -z "$SKIP_SETUP_NCU" ]; then
   KIND=${KIND:-hetero}; N=${N:-200}
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:afsai_setup_rows -s 1 -c 1 \
-     -o /tmp/ncu/setup_$TAG -f python scripts/prof_setup.py $KIND $N 2 > gpurun_out/${TAG}_ncu_setup.log 2>&1
+  # every set-up launch of ONE afsai_setup (table-probe passes, the main pass, retries);
+  # the summary picks the longest (the main pass)
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:afsai_setup_rows -c 8 \
+     -o /tmp/ncu/setup_$TAG -f python scripts/prof_setup.py $KIND $N 1 > gpurun_out/${TAG}_ncu_setup.log 2>&1
   echo "ncu-setup $?"
   ncu -i /tmp/ncu/setup_$TAG.ncu-rep --page raw --csv > gpurun_out/${TAG}_setup_raw.csv 2>&1
   ncu -i /tmp/ncu/setup_$TAG.ncu-rep --page details --csv > gpurun_out/${TAG}_setup_details.csv 2>&1
   ncu -i /tmp/ncu/setup_$TAG.ncu-rep --page source --csv --print-source cuda > gpurun_out/${TAG}_setup_source.csv 2>&1
   python scripts/ncu_summary.py gpurun_out/${TAG}_setup_details.csv gpurun_out/${TAG}_setup_raw.csv \
      > gpurun_out/${TAG}_setup_summary.txt 2>&1
-  python scripts/ncu_lines.py /tmp/ncu/setup_$TAG.ncu-rep "" 60 > gpurun_out/${TAG}_setup_lines.txt 2>&1
+  python scripts/ncu_source_lines.py /tmp/ncu/setup_$TAG.ncu-rep afsai_setup_rows 60 > gpurun_out/${TAG}_setup_lines.txt 2>&1
+  python scripts/ncu_traffic.py gpurun_out/${TAG}_setup_raw.csv $WL > gpurun_out/${TAG}_setup_traffic_$WL.json 2>&1
   gzip -f gpurun_out/${TAG}_setup_source.csv gpurun_out/${TAG}_setup_raw.csv
 fi
 if [ -z "$SKIP_SPMV_NCU" ]; then
