@@ -387,46 +387,34 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = 0x7fffffff; bt[q] = -1; }
             if (running) {
                 const int hw = bk.hw;
-                // two active slots per iteration: their hit folds are independent chains
-                // (interleaved, so the shared-memory and L1/L2 latencies overlap); the
-                // top-GS list is a top-k under a total order, so insertion order is free
-                for (int aa0 = gl; aa0 < hw; aa0 += 2 * LPR) {
-                    int aas[2] = {aa0, aa0 + LPR};
-                    int n[2];
-                    real acc[2] = {real(0), real(0)};
-#pragma unroll
-                    for (int x = 0; x < 2; ++x) n[x] = aas[x] < hw ? w.ahn[aas[x]] : 0;  // 0: a freed slot
+                for (int aa = gl; aa < hw; aa += LPR) {
+                    const int n = w.ahn[aa];  // 0: a freed slot (acc stays +0.0)
+                    real acc = real(0);
 #pragma unroll
                     for (int h = 0; h < HC; ++h) {
-#pragma unroll
-                        for (int x = 0; x < 2; ++x) {
-                            if (h < n[x]) {
-                                const int q = w.ahq[h * CA + aas[x]];
-                                const real gv = q < 0 ? real(1) : w.g[q];
-                                acc[x] = fma(AFSAI_HITVAL(a, w.hv[h * CA + aas[x]]), gv, acc[x]);
-                            }
+                        if (h < n) {
+                            const int q = w.ahq[h * CA + aa];
+                            const real gv = q < 0 ? real(1) : w.g[q];
+                            acc = fma(AFSAI_HITVAL(a, w.hv[h * CA + aa]), gv, acc);
                         }
                     }
+                    c_gfma += n;
+                    // branch-free insertion into the sorted top-GS list (selects)
+                    const bool cand = acc != real(0);
+                    nc += cand;
+                    real ca = cand ? fabs(acc) : -real(1);
+                    int32_t cj = cand ? w.akey[aa] : 0x7fffffff, ct = aa;
 #pragma unroll
-                    for (int x = 0; x < 2; ++x) {
-                        c_gfma += n[x];
-                        // branch-free insertion into the sorted top-GS list (selects)
-                        const bool cand = acc[x] != real(0);
-                        nc += cand;
-                        real ca = cand ? fabs(acc[x]) : -real(1);
-                        int32_t cj = cand ? w.akey[aas[x]] : 0x7fffffff, ct = aas[x];
-#pragma unroll
-                        for (int q = 0; q < GS; ++q) {
-                            const bool b = better(ca, cj, ba[q], bj[q]);
-                            const real ta = ba[q];
-                            const int32_t tj = bj[q], t2 = bt[q];
-                            ba[q] = b ? ca : ba[q];
-                            bj[q] = b ? cj : bj[q];
-                            bt[q] = b ? ct : bt[q];
-                            ca = b ? ta : ca;
-                            cj = b ? tj : cj;
-                            ct = b ? t2 : ct;
-                        }
+                    for (int q = 0; q < GS; ++q) {
+                        const bool b = better(ca, cj, ba[q], bj[q]);
+                        const real ta = ba[q];
+                        const int32_t tj = bj[q], t2 = bt[q];
+                        ba[q] = b ? ca : ba[q];
+                        bj[q] = b ? cj : bj[q];
+                        bt[q] = b ? ct : bt[q];
+                        ca = b ? ta : ca;
+                        cj = b ? tj : cj;
+                        ct = b ? t2 : ct;
                     }
                 }
             }
