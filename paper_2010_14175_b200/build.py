@@ -60,12 +60,14 @@ def _is_contract(src: str) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, debug: bool = False, variant: str = "",
-          defines: tuple = ()) -> str:
+          defines: tuple = (), fp32: bool = True) -> str:
     """variant + defines: an A/B build (extra -D flags) into build_obj_<variant>/ and
     lib/libafsai_b200_<variant>.so, loaded with AFSAI_LIB=<path>."""
     objdir = OBJDIR_DBG if debug else OBJDIR
     lib_out = LIB_DBG if debug else LIB
     extra = ["-DAFSAI_BOUNDS_CHECK"] if debug else []
+    if not fp32:
+        extra = extra + ["-DAFSAI_NO_FP32"]
     if variant:
         objdir = os.path.join("/tmp", "afsai_build_obj_" + variant)  # outside the repo (gpurun snapshot size)
         lib_out = os.path.join(LIBDIR, f"libafsai_b200_{variant}.so")
@@ -80,7 +82,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, varia
     objs, todo = [], []
     for s in srcs:
         # set-up units twice: fp64 (afsai::dp) and fp32 (afsai::sp, -DAFSAI_SETUP_FP32)
-        variants = [("", [])] + ([(".f32", ["-DAFSAI_SETUP_FP32"])] if _is_contract(s) else [])
+        variants = [("", [])] + ([(".f32", ["-DAFSAI_SETUP_FP32"])] if fp32 and _is_contract(s) else [])
         for suffix, vflags in variants:
             o = os.path.join(objdir, os.path.basename(s) + suffix + ".o")
             objs.append(o)
@@ -118,4 +120,4 @@ if __name__ == "__main__":
     var = next((x.split("=", 1)[1] for x in sys.argv if x.startswith("--variant=")), "")
     defs = tuple(x[2:] for x in sys.argv if x.startswith("-D"))
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv,
-                variant=var, defines=defs))
+                variant=var, defines=defs, fp32="--no-fp32" not in sys.argv))

@@ -156,6 +156,17 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     NvtxRange nv("afsai set-up rows kernel");
     // the kernel instances of the set-up precision (afsai::dp fp64, afsai::sp fp32)
     const bool f32 = p.precision == AFSAI_PREC_FP32;
+#ifdef AFSAI_NO_FP32  // a build without the afsai::sp instances (build.py fp32=False, the debug build)
+    if (f32) return set_status(status, AFSAI_ELIMIT, "this build of the library has no fp32 set-up kernels");
+    namespace kp = dp;
+    auto scan_kernel_for = kp::scan_kernel_for;
+    auto scan_row_bytes = kp::scan_row_bytes;
+    auto hits_kernel_for = kp::hits_kernel_for;
+    auto hits_row_bytes = kp::hits_row_bytes;
+    auto lockstep_kernel_for = kp::lockstep_kernel_for;
+    auto prow_kernel_for = kp::prow_kernel_for;
+    auto prow_row_bytes = kp::prow_row_bytes;
+#else
     auto scan_kernel_for = f32 ? sp::scan_kernel_for : dp::scan_kernel_for;
     auto scan_row_bytes = f32 ? sp::scan_row_bytes : dp::scan_row_bytes;
     auto hits_kernel_for = f32 ? sp::hits_kernel_for : dp::hits_kernel_for;
@@ -163,6 +174,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     auto lockstep_kernel_for = f32 ? sp::lockstep_kernel_for : dp::lockstep_kernel_for;
     auto prow_kernel_for = f32 ? sp::prow_kernel_for : dp::prow_kernel_for;
     auto prow_row_bytes = f32 ? sp::prow_row_bytes : dp::prow_row_bytes;
+#endif
     DevBuf val32;  // A_s = single(A) (fp32 set-up)
     if (f32) {
         AFSAI_CUDA_TRY(val32.alloc(std::max<int64_t>(Aext.nnz, 1) * sizeof(float), ctx->stream));

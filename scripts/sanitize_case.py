@@ -1,5 +1,6 @@
-"""Small set-up + apply + PCG cases for compute-sanitizer (tests/test_sanitizer.py):
-every kernel plan (lockstep, hits, pattern-row, scan, the retry path), fp64 and fp32."""
+"""Small set-up + apply + PCG cases over every kernel plan (lockstep, hits, pattern-row,
+scan, the retry path), fp64 and fp32 (fp64 only with AFSAI_CASES_FP64_ONLY=1); run with the
+bounds-checked library by tests/test_bounds_checked.py."""
 import os
 import sys
 
@@ -13,7 +14,7 @@ ctx = Context()
 cases = [(ai.poisson2d(32, 32), 10, 1, 1 << 30), (ai.poisson3d(16), 20, 2, 1 << 30),
          (ai.poisson3d(8), 4, 5, 1 << 30), (ai.fe_elasticity(4), 30, 3, 100),
          (ai.random_sparse_spd(1500, 10, sub=4), 6, 5, 12)]
-for prec in ("fp64", "fp32"):
+for prec in ("fp64",) if os.environ.get("AFSAI_CASES_FP64_ONLY") else ("fp64", "fp32"):
     for A, k, s, cap in cases:
         F = Factor(ctx, DeviceCSR.from_numpy(A), k, s, 0.0, cap, precision=prec)
         b, _ = ai.rhs_for(A)
