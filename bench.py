@@ -335,7 +335,8 @@ def main():
     if setup_ms >= max(ms_G, ms_T) / args.steps:
         achieved = setup_flop / (setup_ms * 1e-3) / 1e12
         # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-        traffic, tfile = None, f"r02_setup_traffic_{wname}.json"
+        traffic = None
+        tfile = f"r02_setup_traffic_{wname}{'' if args.precision == 'fp64' else '_fp32'}.json"
         try:
             traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))["dram_bytes_per_launch"]
         except Exception:

@@ -1012,7 +1012,30 @@ int local_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const d
         KTimer kt(ctx, AFSAI_K_VECTOR);
         launch_pcg_init(n, bd, xd, r, parts, cnt, S, grid, st);
     }
-    launch_apply_local(ctx, F, r, t, z, 3, r, &W);  // z = M^-1 r, rz = r.z
+    // z = M^-1 r = G^T (G r): two deterministic SpMVs (G, then G^T with the fused
+    // r.z), or with AFSAI_APPLY=single one pass over G with fp64 reductions into z
+    // (12 instead of 24 bytes per nonzero), then r.z
+    const char *apply_env = std::getenv("AFSAI_APPLY");
+    const bool single = apply_env && std::strcmp(apply_env, "single") == 0;
+    const int wG1 = spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1), 1);
+    auto apply_rz = [&](int first) {
+        if (single) {
+            cudaMemsetAsync(z, 0, n * sizeof(double), st);
+            {
+                KTimer kt(ctx, AFSAI_K_SPMV_G);
+                launch_apply_single_pass(n, F->g_rowptr.as<int64_t>(), F->g_col.as<int32_t>(), F->g_val.as<double>(),
+                                         r, z, S, wG1, grid, st);
+            }
+            {
+                KTimer kt(ctx, AFSAI_K_VECTOR);
+                launch_pcg_rz(n, r, z, parts, cnt, S, first, grid, st);
+            }
+            ctx->launches += 2;
+        } else {
+            launch_apply_local(ctx, F, r, t, z, first ? 3 : 2, r, &W);
+        }
+    };
+    apply_rz(1);  // z = M^-1 r, rz = r.z
     {
         KTimer kt(ctx, AFSAI_K_VECTOR);
         launch_pcg_update_p(n, p, z, S, 1, grid, st);  // p = z
@@ -1036,7 +1059,7 @@ int local_pcg(afsai_ctx_t ctx, const afsai_csr_t *Ain, afsai_factor_t F, const d
                 KTimer kt(ctx, AFSAI_K_VECTOR);
                 launch_pcg_axpy(n, xd, r, p, q, parts, cnt, S, tol, max_iters, grid, st);  // x, r, test
             }
-            launch_apply_local(ctx, F, r, t, z, 2, r, &W);  // z = M^-1 r, beta
+            apply_rz(0);  // z = M^-1 r, beta
             {
                 KTimer kt(ctx, AFSAI_K_VECTOR);
                 launch_pcg_update_p(n, p, z, S, 0, grid, st);  // p = z + beta p

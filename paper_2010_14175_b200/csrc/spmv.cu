@@ -339,6 +339,84 @@ void launch_pcg_update_p_dist(int64_t n, double *p, const double *z, PcgState *s
 }
 void launch_pcg_rz_dist(PcgState *st, cudaStream_t s) { pcg_rz_dist_kernel<<<1, 1, 0, s>>>(st); }
 
+// ---------------------------------------------------------------- single-pass apply
+// z += G^T (G r) reading G once: row i computes t_i = g_i . r
+// (the miniwarp fold of spmv_kernel, same order) and scatters t_i * G_ij into
+// z_j with fp64 reductions in L2 (RED.ADD.F64: no return value).  12 B per
+// nonzero of G instead of the two-pass 24 B; the order of the additions into
+// z_j is not fixed (non-deterministic rounding, within the +-1 PCG-iteration
+// rule).  z must be zero on entry.
+template <int W>
+__global__ void __launch_bounds__(256) apply_single_pass_kernel(int64_t n, const int64_t *rowptr, const int32_t *col,
+                                                                const double *val, const double *r, double *z,
+                                                                const PcgState *st) {
+    if (st && st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & (W - 1);
+    constexpr int RPW = 32 / W;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r0 = warp * RPW; r0 < n; r0 += nwarps * RPW) {
+        const int64_t row = r0 + lane / W;
+        double acc = 0.0;
+        int64_t e0 = 0, e1 = 0;
+        if (row < n) {
+            e0 = rowptr[row];
+            e1 = rowptr[row + 1];
+            int64_t e = e0 + sub;
+            for (; e + 3 * W < e1; e += 4 * W) {
+                int32_t c[4];
+                double v[4], xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    c[u] = __ldg(col + e + u * W);
+                    v[u] = __ldg(val + e + u * W);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = __ldg(r + c[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc = fma(v[u], xv[u], acc);
+            }
+            for (; e < e1; e += W) acc = fma(__ldg(val + e), __ldg(r + __ldg(col + e)), acc);
+        }
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFullS, acc, o);  // every lane: t_row
+        if (row < n)
+            for (int64_t e = e0 + sub; e < e1; e += W) atomicAdd(z + __ldg(col + e), __ldg(val + e) * acc);
+    }
+}
+
+// r.z (z complete) -> beta = (r,z)_new / (r,z)_old, rz (the MODE 2 update of spmv_kernel)
+__global__ void __launch_bounds__(256) pcg_rz_kernel(int64_t n, const double *r, const double *z, double *partials,
+                                                     unsigned *counter, PcgState *st, int first) {
+    __shared__ double sh[32];
+    if (st->done) return;
+    double s = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        s = fma(z[k], r[k], s);
+    double tot;
+    if (grid_reduce_last(s, partials, counter, sh, &tot)) {
+        if (!first) st->beta = tot / st->rz;
+        st->rz = tot;
+    }
+}
+
+void launch_apply_single_pass(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
+                              const double *r, double *z, const PcgState *st, int width, int grid, cudaStream_t s) {
+    switch (width) {
+        case 1: apply_single_pass_kernel<1><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+        case 2: apply_single_pass_kernel<2><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+        case 4: apply_single_pass_kernel<4><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+        case 8: apply_single_pass_kernel<8><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+        case 16: apply_single_pass_kernel<16><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+        default: apply_single_pass_kernel<32><<<grid, 256, 0, s>>>(n, rowptr, col, val, r, z, st); break;
+    }
+}
+void launch_pcg_rz(int64_t n, const double *r, const double *z, double *partials, unsigned *counter, PcgState *st,
+                   int first, int grid, cudaStream_t s) {
+    pcg_rz_kernel<<<grid, 256, 0, s>>>(n, r, z, partials, counter, st, first);
+}
+
 // ---------------------------------------------------------------- fp64 FMA probe
 // Independent DFMA chains per thread (8 accumulators), enough warps to fill
 // every SMSP: the measured fp64 roofline denominator of the set-up.

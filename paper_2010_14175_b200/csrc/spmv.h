@@ -42,6 +42,12 @@ void launch_pcg_update_p(int64_t n, double *p, const double *z, const PcgState *
 void launch_residual(int64_t n, const double *b, const double *ax, double *partials, unsigned *counter, double *out,
                      int grid, cudaStream_t s);
 void launch_dfma_probe(double *out, int iters, int grid, cudaStream_t s);
+// single-pass apply z += G^T (G r) (z zero on entry; fp64 reductions, non-deterministic order)
+void launch_apply_single_pass(int64_t n, const int64_t *rowptr, const int32_t *col, const double *val,
+                              const double *r, double *z, const PcgState *st, int width, int grid, cudaStream_t s);
+// rz = r.z and beta = rz / rz_old (first: rz only)
+void launch_pcg_rz(int64_t n, const double *r, const double *z, double *partials, unsigned *counter, PcgState *st,
+                   int first, int grid, cudaStream_t s);
 // multi-GPU PCG pieces (scalars from all-reduced st->sum[])
 void launch_pcg_init_dist(int64_t n, const double *b, double *x, double *r, double *partials, unsigned *counter,
                           PcgState *st, int grid, cudaStream_t s);      // sum[1] = local b.b

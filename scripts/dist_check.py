@@ -86,6 +86,22 @@ for name, A, k, s, cap in [("poisson3d_24", ai.poisson3d(24), 20, 2, 1000), ("fe
                                          "iters_N": rep["iters"], "converged": bool(rep["converged"]),
                                          "halo_rows": st["halo_rows"], "halo_bytes": st["halo_bytes"]}
         F.close()
+# fp32 set-up on N GPUs against the fp32 oracle
+for name, A, k, s, cap in [("hetero_16", ai.hetero_poisson3d(16), 20, 2, 1000), ("fe_7", ai.fe_elasticity(7), 30, 3, 100)]:
+    n = A.n
+    bounds = [n * q // world for q in range(world + 1)]
+    b, e = bounds[rank], bounds[rank + 1]
+    Gr = oracle.setup(A, k, s, 0.0, cap, precision="fp32").to_csr(n)
+    F = Factor(ctx, DeviceCSR.from_numpy(A, row_begin=b, n_rows=e - b), k, s, 0.0, cap, precision="fp32")
+    rp, ci, v = (t.cpu().numpy() for t in F.G())
+    a0, a1 = Gr.rowptr[b], Gr.rowptr[e]
+    ok = (np.array_equal(rp, Gr.rowptr[b:e + 1] - a0) and np.array_equal(ci, Gr.col[a0:a1])
+          and np.array_equal(v.view(np.int64), Gr.val[a0:a1].view(np.int64)))
+    bvec, _ = ai.rhs_for(A)
+    x, rep = F.pcg(torch.from_numpy(bvec[b:e].copy()).cuda(), tol=1e-8, max_iters=5000)
+    results[f"{name}_fp32"] = {"G_bitwise_vs_oracle": bool(ok), "converged": bool(rep["converged"]),
+                               "iters_N": rep["iters"], "stripes": [], "oracle_stripes": []}
+    F.close()
 # error agreement: row n-1 has a tiny diagonal (psi < 0 at step 1 on the last rank only)
 B = ai.poisson3d(12)
 val = B.val.copy()
@@ -112,9 +128,9 @@ dist.all_gather_object(allr, results)
 if rank == 0:
     ok = all(r[c]["G_bitwise_vs_oracle"] and r[c]["Gt_bitwise_vs_oracle"] and r[c]["apply_within_bound_vs_oracle"]
              and abs(r[c]["iters_N"] - r[c]["iters_oracle"]) <= 1 and r[c]["true_rel_res"] <= 1e-7
-             for r in allr for c in r if c != "error_agreement" and "_halo_k" not in c)
+             for r in allr for c in r if c != "error_agreement" and "_halo_k" not in c and "_fp32" not in c)
     ok = ok and all(r[c]["G_bitwise_vs_oracle"] and r[c]["converged"] and r[c]["stripes"] == r[c]["oracle_stripes"]
-                    for r in allr for c in r if "_halo_k" in c)
+                    for r in allr for c in r if "_halo_k" in c or "_fp32" in c)
     ok = ok and all(r["error_agreement"]["ok"] for r in allr) and allr[0]["error_agreement"]["oracle_code"] == 2
     print(json.dumps({"world": world, "ok": ok, "ranks": allr}, indent=1))
 dist.destroy_process_group()

@@ -249,6 +249,25 @@ def test_pcg_parity(ctx, make, k, s, cap):
     F.close()
 
 
+@pytest.mark.parametrize("make,k,s,cap", [(lambda: ai.poisson3d(16), 20, 2, 1 << 30),
+                                          (lambda: ai.hetero_poisson3d(12), 20, 2, 1 << 30),
+                                          (lambda: ai.fe_elasticity(6), 30, 3, 100)])
+def test_pcg_single_pass_apply(ctx, make, k, s, cap, monkeypatch):
+    """AFSAI_APPLY=single: M^-1 r in one pass over G with fp64 reductions (non-deterministic
+    summation order): PCG iterations within 1 of the oracle, solution to 1e-6."""
+    monkeypatch.setenv("AFSAI_APPLY", "single")
+    A = make()
+    b, xs = ai.rhs_for(A)
+    F = gpu_setup(ctx, A, k, s, 0.0, cap)
+    x, rep = F.pcg(torch.from_numpy(b).cuda(), tol=1e-8, max_iters=5000)
+    G, Gt, _ = oracle.setup_full(A, k, s, 0.0, cap)
+    pr = oracle.pcg(A, G, Gt, b, tol=1e-8, max_iters=5000)
+    assert rep["converged"] and abs(rep["iters"] - pr.iters) <= 1, (rep["iters"], pr.iters)
+    assert rep["true_rel_res"] <= 10 * 1e-8
+    assert np.linalg.norm(x.cpu().numpy() - pr.x) <= 1e-6 * np.linalg.norm(pr.x)
+    F.close()
+
+
 def test_pcg_identity_and_host_buffers(ctx):
     I = ai.diagonal(np.ones(100))
     b = ai.rng("vectors", 13).standard_normal(100)
