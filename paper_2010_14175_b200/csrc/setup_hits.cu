@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
             const bool vi = gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
             const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
-            scan_row_hits<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, (int32_t)(e0i + gl), -1, nullptr, nullptr);
+            scan_row_hits<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, G.gl, -1, nullptr, nullptr);
         }
         const real a_ii = w.dscr[0];
         const real psi0 = a_ii;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                     if (h < n) {
                         const int q = w.ahq[h * CA + aa];
                         const real gv = q < 0 ? real(1) : w.g[q];
-                        acc = fma(AFSAI_HITVAL(a, w.hv[h * CA + aa]), gv, acc);
+                        acc = fma(__ldg(aval(a) + (q < 0 ? e0i : (int64_t)w.prs[q]) + w.hv[h * CA + aa]), gv, acc);
                     }
                 }
                 c_gfma += n;
@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
                 w.hval[w.ahs[aa]] = (int8_t)(m + rank);
                 const int64_t g0 = rp_of(a, j), g1 = rp_of(a, (int64_t)j + 1);
                 w.gstart[rank] = g0;
+                w.prs[m + rank] = (int32_t)g0;
                 w.glen[rank] = (int32_t)(g1 - g0);
                 w.ahn[aa] = 0;
                 w.afree[w.misc[3] + gl] = (int16_t)aa;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(256, (LPR == 32 ? 2 : 1)) afsai_setup_rows_hit
 #pragma unroll
                 for (int u = 0; u < GS; ++u) {  // every row's entries in flight at once
                     pvld[u] = (ug + u < nsel) && gl < w.glen[ug + u];
-                    pe[u] = (int32_t)(w.gstart[ug + u] + gl);
+                    pe[u] = gl;   // the entry's position within its row
                     pc[u] = pvld[u] ? __ldg(a.col + w.gstart[ug + u] + gl) : 0;
                     pv[u] = pvld[u] ? __ldg(aval(a) + w.gstart[ug + u] + gl) : real(0);
                 }

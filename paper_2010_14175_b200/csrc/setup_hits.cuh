@@ -6,19 +6,20 @@
 namespace afsai {
 namespace AFSAI_PNS {
 
-// A recorded hit (candidate j, pattern row r) is the int32 index of the entry
-// (r, j) in A's arrays, not the value a_jr: 4 bytes instead of 8 per hit, so more
-// rows fit in shared memory (M3: 14 -> 16 rows per SM); the gradient re-reads the
-// value (an L1/L2 hit, the same bits).  Needs nnz(A_ext) < 2^31 (run_rows).
-typedef int32_t hit_t;
-#define AFSAI_HIT(v, e) (e)
-#define AFSAI_HITVAL(a, h) __ldg(aval(a) + (h))
+// A recorded hit (candidate j, pattern row r = P_q) is the position of the entry
+// (r, j) within row r (rows of the hit-list plans hold <= 16 entries: one int8),
+// not the value a_jr: with the start of each pattern row kept once per position
+// (prs[q], int32; row i's start is a register) the gradient re-reads the value
+// (an L1/L2 hit, the same bits) -- 1 byte per hit instead of 8, so more rows fit
+// in shared memory.  Needs nnz(A_ext) < 2^31 (run_rows).
+typedef int8_t hit_t;
+#define AFSAI_HIT(v, off) ((int8_t)(off))
 
 struct HitState {
     real *inv, *y, *g, *L, *arow, *brow, *dscr, *acc;
     hit_t *hv;
     int64_t *gstart;
-    int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey;
+    int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey, *prs;
     int16_t *ahs, *afree;
     int8_t *hval, *ahn, *ahq;
     int M, CA;
@@ -28,9 +29,9 @@ template <int HC>
 __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc) {
     int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (acc ? CA : 0);
     int64_t i64 = S;
-    int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA + (int64_t)CA * HC;  // ... akey, hv
+    int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA + M;  // ... akey, prs
     int64_t i16 = 2 * (int64_t)CA;
-    int64_t i8 = (int64_t)H + CA + (int64_t)CA * HC;
+    int64_t i8 = (int64_t)H + CA + 2 * (int64_t)CA * HC;  // hval, ahn, ahq, hv
     int64_t b = real_bytes(dbl) + i64 * 8 + i32 * 4 + i16 * 2 + i8;
     return (b + 15) & ~int64_t(15);
 }
@@ -63,14 +64,15 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.glen = ip; ip += S;
     w.misc = ip; ip += 8;
     w.akey = ip; ip += CA;
-    w.hv = ip; ip += CA * HC;  // [h][a]
+    w.prs = ip; ip += M;
     int16_t *sp = reinterpret_cast<int16_t *>(ip);
     w.ahs = sp; sp += CA;
     w.afree = sp; sp += CA;
     int8_t *bp = reinterpret_cast<int8_t *>(sp);
     w.hval = bp; bp += H;
     w.ahn = bp; bp += CA;
-    w.ahq = bp;  // [h][a]
+    w.ahq = bp; bp += CA * HC;  // [h][a]
+    w.hv = bp;                  // [h][a]
     return w;
 }
 

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             const bool vi = has && gl < (int)(e1i - e0i);
             const int32_t ci = vi ? __ldg(a.col + e0i + gl) : 0;
             const real xi = vi ? __ldg(aval(a) + e0i + gl) : real(0);
-            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, (int32_t)(e0i + gl), -1, nullptr, nullptr, bk);
+            scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, vi, ci, xi, gl, -1, nullptr, nullptr, bk);
         }
         const real a_ii = w.dscr[0];
         const real psi0 = a_ii;
@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                         if (h < n) {
                             const int q = w.ahq[h * CA + aa];
                             const real gv = q < 0 ? real(1) : w.g[q];
-                            acc = fma(AFSAI_HITVAL(a, w.hv[h * CA + aa]), gv, acc);
+                            const int64_t rb = q < 0 ? e0i : (int64_t)w.prs[q];
+                            acc = fma(__ldg(aval(a) + rb + w.hv[h * CA + aa]), gv, acc);
                         }
                     }
                     c_gfma += n;
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             //      registers, the winner's lane stores its slot and row extent
             int32_t selj[GS];
             int32_t pc[GS], pe[GS];
+            int64_t g0s[GS];
             real pv[GS];
             bool pvld[GS];
 #pragma unroll
@@ -469,7 +471,8 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     const int gn = G.bcast((int)(re[0] - rs[0]), wl);
                     pvld[u] = (u < nsel) && gl < gn;
                     pc[u] = pvld[u] ? __ldg(a.col + g0 + gl) : 0;
-                    pe[u] = (int32_t)(g0 + gl);
+                    pe[u] = gl;   // the entry's position within its row
+                    g0s[u] = g0;
                     pv[u] = pvld[u] ? __ldg(aval(a) + g0 + gl) : real(0);
                     if (won) {
                         w.sela[u] = bt[0];
@@ -502,11 +505,13 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
             if (gl < nsel) {
                 int32_t j = selj[0];
                 int r = rk[0];
+                int64_t g0 = g0s[0];
 #pragma unroll
                 for (int u = 1; u < GS; ++u)
-                    if (gl == u) { j = selj[u]; r = rk[u]; }
+                    if (gl == u) { j = selj[u]; r = rk[u]; g0 = g0s[u]; }
                 const int aa = w.sela[gl];
                 w.P[m + r] = j;
+                w.prs[m + r] = (int32_t)g0;
                 w.hval[w.ahs[aa]] = (int8_t)(m + r);
                 w.ahn[aa] = 0;
                 w.afree[bk.nf + gl] = (int16_t)aa;
