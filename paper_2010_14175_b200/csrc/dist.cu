@@ -25,6 +25,7 @@
 #include <cmath>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "assemble.h"
@@ -228,6 +229,11 @@ int block_rows_to_G(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_
     return AFSAI_OK;
 }
 
+// out[k] = in[idx[k]] (a few scattered values of a device array for the host)
+__global__ void gather_i64_kernel(const int64_t *in, const int64_t *idx, int n, int64_t *out) {
+    for (int k = threadIdx.x; k < n; k += blockDim.x) out[k] = in[idx[k]];
+}
+
 // Gather rows [lo, b) of A from lower ranks (exact set-up halo) and build the
 // extended CSR of rows [lo, e).
 static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<int64_t> &bounds, int64_t lo,
@@ -260,9 +266,24 @@ static int gather_halo(afsai_ctx_t ctx, const DeviceCsr &A, const std::vector<in
         AFSAI_NCCL_TRY(range_exchange(P1, len.p, sizeof(int32_t), ctx->comm, st));
     }
     AFSAI_CUDA_TRY(exclusive_scan(len.as<int32_t>(), next, rp.as<int64_t>(), tiles.as<int64_t>(), st, &ctx->launches));
-    std::vector<int64_t> hrp(next + 1);
-    AFSAI_CUDA_TRY(cudaMemcpyAsync(hrp.data(), rp.p, (next + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    // the host needs the extended row pointer only at segment boundaries (entry
+    // ranges of the sends / receives), at b and at the end: gather those few values
+    // on the device instead of copying the whole (n_rows + halo) row pointer
+    std::vector<int64_t> need = {next, b - lo};
+    for (const Seg &sg : P.recvs) need.insert(need.end(), {sg.begin - lo, sg.begin + sg.count - lo});
+    for (const Seg &sg : P.sends) need.insert(need.end(), {sg.begin - lo, sg.begin + sg.count - lo});
+    DevBuf dneed;
+    AFSAI_CUDA_TRY(dneed.alloc(2 * need.size() * sizeof(int64_t), st));
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(dneed.p, need.data(), need.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    gather_i64_kernel<<<1, 256, 0, st>>>(rp.as<int64_t>(), dneed.as<int64_t>(), (int)need.size(),
+                                         dneed.as<int64_t>() + need.size());
+    ctx->launches += 1;
+    std::vector<int64_t> vals(need.size());
+    AFSAI_CUDA_TRY(cudaMemcpyAsync(vals.data(), dneed.as<int64_t>() + need.size(), need.size() * sizeof(int64_t),
+                                   cudaMemcpyDeviceToHost, st));
     AFSAI_CUDA_TRY(cudaStreamSynchronize(st));
+    std::unordered_map<int64_t, int64_t> hrp;  // extended row index -> entry offset
+    for (size_t k = 0; k < need.size(); ++k) hrp[need[k]] = vals[k];
     const int64_t nnz_ext = hrp[next];
     // stage 2: col / val of the halo rows straight into the extended arrays;
     // sends come from my local arrays (entry ranges from my host row pointer)
