@@ -195,7 +195,6 @@ struct afsai_factor_s {
     int64_t nnz_G = 0;
     // G^T: local rows (global row index row_begin + k), global columns
     afsai::DevBuf t_rowptr, t_col, t_val;
-    afsai::DevBuf t_perm;  // G^T rows sorted by length within windows of 64 (SpMV row order)
     int64_t nnz_Gt = 0;
     // per-row trace
     afsai::DevBuf steps, reason;

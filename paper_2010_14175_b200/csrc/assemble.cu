@@ -359,35 +359,6 @@ void sort_gt_rows(int64_t n_rows, const int64_t *rowptr, int32_t *in_col, double
     *launches += 2;
 }
 
-// Row order for the SpMV of an irregular CSR (G^T: row lengths vary, mean 41, up to
-// ~3.5x that on M3): within each window of 64 consecutive rows, rows sorted by length
-// (descending, then index), so the rows sharing a warp have similar lengths while
-// the x-gathers keep their locality.  One warp per window.
-__global__ void window_len_perm_kernel(int64_t n_rows, const int64_t *rowptr, int32_t *perm) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t w0 = warp * 64; w0 < n_rows; w0 += nw * 64) {
-        const int cnt = (int)(n_rows - w0 < 64 ? n_rows - w0 : 64);
-        int64_t len[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int k = lane + 32 * h;
-            len[h] = k < cnt ? rowptr[w0 + k + 1] - rowptr[w0 + k] : -1;
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int k = lane + 32 * h;
-            int rank = 0;
-            for (int m = 0; m < cnt; ++m) {
-                const int64_t lm = __shfl_sync(0xffffffffu, (m >> 5) ? len[1] : len[0], m & 31);
-                rank += (lm > len[h]) || (lm == len[h] && m < k);
-            }
-            if (k < cnt) perm[w0 + rank] = (int32_t)(w0 + k);
-        }
-    }
-}
-
 // ---------------------------------------------------------------- multi-GPU helpers
 // lengths of local rows (int32) from a row pointer
 __global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len) {

@@ -24,7 +24,6 @@ __global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const in
 // sort every row of a scattered G^T by source row (C10); in_* is clobbered
 void sort_gt_rows(int64_t n_rows, const int64_t *rowptr, int32_t *in_col, double *in_val, int32_t *out_col,
                   double *out_val, int grid, cudaStream_t st, int64_t *launches);
-__global__ void window_len_perm_kernel(int64_t n_rows, const int64_t *rowptr, int32_t *perm);
 __global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len);
 __global__ void g_triples_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
                                  int64_t row_begin, int32_t *tc, int32_t *tr, double *tv);

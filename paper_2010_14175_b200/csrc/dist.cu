@@ -470,9 +470,6 @@ static int dist_transpose(afsai_ctx_t ctx, afsai_factor_t F, const std::vector<i
     dt.mark("scatter");
     sort_gt_rows(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(), F->t_col.as<int32_t>(),
                  F->t_val.as<double>(), grid, st, &ctx->launches);
-    AFSAI_CUDA_TRY(F->t_perm.alloc(std::max<int64_t>(n_out, 1) * sizeof(int32_t), st));
-    window_len_perm_kernel<<<grid, 256, 0, st>>>(n_out, F->t_rowptr.as<int64_t>(), F->t_perm.as<int32_t>());
-    ctx->launches += 1;
     dt.mark("sort");
     ctx->launches += 2;
     AFSAI_CUDA_TRY(cudaGetLastError());
@@ -818,7 +815,6 @@ static int dist_apply_ext(afsai_ctx_t ctx, afsai_factor_t F, double *re, double 
     }
     SpmvArgs c = sargs(n, F->t_rowptr.as<int64_t>(), F->t_col.as<int32_t>(), F->t_val.as<double>(), te, D->planT.lo,
                        z);
-    if (F->t_perm.p && !std::getenv("AFSAI_NO_GT_PERM")) c.perm = F->t_perm.as<int32_t>();
     int mode = 0;
     if (pw) {
         c.st = pw->state.as<PcgState>();

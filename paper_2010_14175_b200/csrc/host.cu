@@ -855,9 +855,7 @@ int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out
                                            tval.as<double>());
     sort_gt_rows(n_out, F->t_rowptr.as<int64_t>(), tcol.as<int32_t>(), tval.as<double>(), F->t_col.as<int32_t>(),
                  F->t_val.as<double>(), grid, st, &ctx->launches);
-    AFSAI_CUDA_TRY(F->t_perm.alloc(std::max<int64_t>(n_out, 1) * sizeof(int32_t), st));
-    window_len_perm_kernel<<<grid, 256, 0, st>>>(n_out, F->t_rowptr.as<int64_t>(), F->t_perm.as<int32_t>());
-    ctx->launches += 2;
+    ctx->launches += 1;
     AFSAI_CUDA_TRY(cudaGetLastError());
     return AFSAI_OK;
 }
@@ -903,7 +901,6 @@ void launch_apply_local(afsai_ctx_t ctx, afsai_factor_t F, const double *r, doub
         launch_spmv(a, 0, spmv_group_width((double)F->nnz_G / std::max<int64_t>(n, 1), 1), grid, ctx->stream);
     }
     SpmvArgs b = spmv_args(n, F->t_rowptr.as<int64_t>(), F->t_col.as<int32_t>(), F->t_val.as<double>(), t, 0, z);
-    if (F->t_perm.p && !std::getenv("AFSAI_NO_GT_PERM")) b.perm = F->t_perm.as<int32_t>();
     if (pw) {
         b.st = pw->state.as<PcgState>();
         b.w = w;

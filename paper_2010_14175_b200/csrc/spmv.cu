@@ -74,10 +74,9 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double dsum = 0.0;
     for (int64_t r0 = warp * RPW; r0 < a.n; r0 += nwarps * RPW) {
-        const int64_t slot = r0 + lane / W;
-        const int64_t row = (a.perm && slot < a.n) ? (int64_t)__ldg(a.perm + slot) : slot;
+        const int64_t row = r0 + lane / W;
         double acc = 0.0;
-        if (slot < a.n) {
+        if (row < a.n) {
             const int64_t e1 = a.rowptr[row + 1];
             int64_t e = a.rowptr[row] + sub;
             // four entries per lane in flight (column loads, then the x gathers),
@@ -99,7 +98,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
         }
 #pragma unroll
         for (int o = W / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFullS, acc, o);
-        if (sub == 0 && slot < a.n) {
+        if (sub == 0 && row < a.n) {
             a.y[row] = acc;
             if (MODE != 0) dsum = fma(acc, a.w[row], dsum);
         }

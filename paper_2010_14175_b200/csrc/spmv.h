@@ -25,7 +25,6 @@ struct SpmvArgs {
     const double *w;         // fused dot partner (mode 1, 2, 3)
     double *partials;        // gridDim.x doubles
     unsigned *counter;       // last-block counter (zero at rest)
-    const int32_t *perm;     // optional row order (G^T: rows sorted by length within windows of 64)
     PcgState *st;            // optional: skip when st->done; scalar updates
     int sum_idx;             // mode 4: local dot stored in st->sum[sum_idx]
 };
