@@ -64,8 +64,8 @@ extern "C" {
 /* A CSR matrix (or a contiguous row block of one).  Columns strictly increasing
  * within each row and GLOBAL; rowptr[0] may be nonzero (offsets are relative to
  * rowptr[0]); the diagonal must be stored.  For afsai_setup A must be SPD and
- * bitwise symmetric (C1); the symmetry check runs only when the
- * environment variable AFSAI_VALIDATE=1. */
+ * bitwise symmetric (C1); the symmetry check (pairs within the rows
+ * held here) runs by default, AFSAI_VALIDATE=0 skips it. */
 typedef struct {
     int64_t n_rows;        /* rows held here                                         */
     int64_t n_cols;        /* global n                                               */

@@ -109,8 +109,11 @@ int validate_csr(afsai_ctx_t ctx, const DeviceCsr &A, int64_t *max_row_len, afsa
                                                         A.n_cols, err.as<unsigned long long>());
     row_len_max_kernel<<<grid, 256, 0, ctx->stream>>>(A.rowptr, A.n_rows, err.as<unsigned long long>() + 1);
     ctx->launches += 2;
+    // bitwise symmetry (contract C1: the hit-list kernels read a_jr from row r) is
+    // checked by default (one binary search per entry; pairs inside this rank's
+    // rows); AFSAI_VALIDATE=0 skips it
     const char *v = std::getenv("AFSAI_VALIDATE");
-    if (v && v[0] == '1') {
+    if (!(v && v[0] == '0')) {
         symmetry_kernel<<<grid, 256, 0, ctx->stream>>>(A.rowptr, A.col, A.val, A.base, A.n_rows, A.row_begin,
                                                        err.as<unsigned long long>());
         ctx->launches += 1;

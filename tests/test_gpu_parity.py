@@ -292,6 +292,13 @@ def test_errors(ctx):
     with pytest.raises(capi.AfsaiError) as e:
         gpu_setup(ctx, ai.CSR(B.n, B.rowptr, col, B.val), 2, 1)
     assert e.value.code == capi.AFSAI_EINVAL
+    # not bitwise symmetric (contract C1): one off-diagonal value moved by one ulp
+    val = B.val.copy()
+    e01 = B.rowptr[0] + 1   # entry (0, 1); (1, 0) keeps the old bits
+    val[e01] = np.nextafter(val[e01], 0.0)
+    with pytest.raises(capi.AfsaiError) as e:
+        gpu_setup(ctx, ai.CSR(B.n, B.rowptr, B.col, val), 2, 1)
+    assert e.value.code == capi.AFSAI_EINVAL and "symmetric" in str(e.value)
     # invalid params
     with pytest.raises(capi.AfsaiError) as e:
         gpu_setup(ctx, B, 2, 0)
