@@ -200,6 +200,13 @@ int afsai_setup_block(afsai_ctx_t ctx, const afsai_csr_t *A_ext, int64_t row_lo,
 int afsai_plan_ranges(int32_t me, int32_t nranks, const int64_t *bounds, const int64_t *lo, const int64_t *hi,
                       int64_t *out, int32_t max_out);
 
+/* Host-only (no GPU): the stripes rank `me` gathers in the bounded-communication
+ * set-up (params.halo_k = k): ahat_rows[q] is row q of the
+ * communication matrix A-hat as a bit mask (bit r set iff a row of stripe q has a
+ * column in stripe r); *mask gets bit q for every q <= me with (A-hat^k)_me,q != 0.
+ * nranks <= 64; returns AFSAI_EINVAL on bad arguments. */
+int afsai_bounded_stripes(int32_t me, int32_t nranks, const uint64_t *ahat_rows, int32_t k, uint64_t *mask);
+
 /* ---- factor access */
 int afsai_factor_nnz(afsai_factor_t F, int64_t *nnz_G, int64_t *nnz_Gt);
 /* Copy the local rows of G (which == 0) or G^T (which == 1) into caller buffers

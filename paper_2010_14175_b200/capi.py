@@ -26,7 +26,7 @@ EXPORTS = [
     "afsai_ctx_rank", "afsai_ctx_destroy", "afsai_setup", "afsai_apply", "afsai_pcg", "afsai_factor_nnz",
     "afsai_factor_copy", "afsai_factor_trace", "afsai_factor_stats", "afsai_factor_retried", "afsai_factor_destroy",
     "afsai_ctx_launches", "afsai_probe_dfma_peak", "afsai_ctx_set_timing", "afsai_ctx_kernel_times",
-    "afsai_setup_block", "afsai_plan_ranges",
+    "afsai_setup_block", "afsai_plan_ranges", "afsai_bounded_stripes",
 ]
 KERNEL_CLASSES = ["setup_rows", "assemble", "transpose", "spmv_G", "spmv_Gt", "spmv_A", "vector", "comm"]
 
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH):
         "afsai_setup_block": ([P, ctypes.POINTER(afsai_csr_t), i64, i64, ctypes.POINTER(afsai_params_t), P,
                                ctypes.POINTER(afsai_status_t)], ctypes.c_int),
         "afsai_plan_ranges": ([i32, i32, P, P, P, P, i32], ctypes.c_int),
+        "afsai_bounded_stripes": ([i32, i32, P, i32, P], ctypes.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)  # AttributeError if the symbol is missing
@@ -312,3 +313,15 @@ def afsai_plan_ranges(me: int, nranks: int, bounds, lo, hi):
         raise AfsaiError(AFSAI_EINVAL, where="afsai_plan_ranges")
     return [("send" if out[4 * t] == 0 else "recv", int(out[4 * t + 1]), int(out[4 * t + 2]), int(out[4 * t + 3]))
             for t in range(k)]
+
+
+def afsai_bounded_stripes(me: int, ahat_rows, k: int) -> list:
+    """Host-only: the stripes q <= me with (A-hat^k)_me,q != 0 (ahat_rows: one int bit mask per rank)."""
+    import numpy as np
+    rows = np.ascontiguousarray(np.asarray(ahat_rows, dtype=np.uint64))
+    mask = ctypes.c_uint64()
+    rc = lib().afsai_bounded_stripes(int(me), len(rows), rows.ctypes.data_as(ctypes.c_void_p), int(k),
+                                     ctypes.byref(mask))
+    if rc:
+        raise AfsaiError(rc, where="afsai_bounded_stripes")
+    return [q for q in range(len(rows)) if (mask.value >> q) & 1]

@@ -520,15 +520,9 @@ static int comm_neighbours(afsai_ctx_t ctx, const DeviceCsr &A, const std::vecto
     std::vector<int64_t> rows;  // A-hat, one bit row per rank
     int rc = allgather_i64(ctx, (int64_t)mine, rows, status);
     if (rc) return rc;
-    uint64_t reach = 1ull << ctx->rank;
-    for (int t = 0; t < k; ++t) {
-        uint64_t nx = reach;
-        for (int q = 0; q < np; ++q)
-            if ((reach >> q) & 1ull) nx |= (uint64_t)rows[q];
-        reach = nx;
-    }
-    const uint64_t lower = ctx->rank == 63 ? ~0ull : ((2ull << ctx->rank) - 1ull);
-    *nmask = reach & lower;
+    std::vector<uint64_t> ur(rows.begin(), rows.end());
+    if (afsai_bounded_stripes(ctx->rank, np, ur.data(), k, nmask) != AFSAI_OK)
+        return set_status(status, AFSAI_EINVAL, "bad communication matrix");
     return AFSAI_OK;
 }
 
@@ -1059,6 +1053,21 @@ int afsai_setup_block(afsai_ctx_t ctx, const afsai_csr_t *Ain, int64_t row_lo, i
         return rc;
     }
     *out = F;
+    return AFSAI_OK;
+}
+
+int afsai_bounded_stripes(int32_t me, int32_t nranks, const uint64_t *ahat_rows, int32_t k, uint64_t *mask) {
+    if (nranks < 1 || nranks > 64 || me < 0 || me >= nranks || k < 0 || !ahat_rows || !mask) return AFSAI_EINVAL;
+    // (A-hat^k)_me,q != 0  <=>  q reachable from me in at most k steps (A-hat has a nonzero diagonal)
+    uint64_t reach = 1ull << me;
+    for (int t = 0; t < k; ++t) {
+        uint64_t nx = reach;
+        for (int q = 0; q < nranks; ++q)
+            if ((reach >> q) & 1ull) nx |= ahat_rows[q];
+        reach = nx;
+    }
+    const uint64_t lower = me == 63 ? ~0ull : ((2ull << me) - 1ull);
+    *mask = reach & lower;
     return AFSAI_OK;
 }
 

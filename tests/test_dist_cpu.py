@@ -89,3 +89,22 @@ def test_plan_ranges_world2_gloo():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_bounded_stripes_host_logic():
+    """afsai_bounded_stripes (the C library's host-side A-hat^k stripe selection of the
+    bounded-communication set-up) against the oracle's plain boolean matrix
+    power on random communication matrices (symmetric, diagonal set)."""
+    import numpy as np
+
+    import oracle
+    from paper_2010_14175_b200 import capi
+    rng = np.random.default_rng(7)
+    for npr in (1, 2, 3, 5, 8, 13):
+        for trial in range(6):
+            H = rng.random((npr, npr)) < 0.25
+            H = H | H.T | np.eye(npr, dtype=bool)
+            rows = [int(sum(1 << q for q in range(npr) if H[p, q])) for p in range(npr)]
+            for k in range(0, 4):
+                for me in range(npr):
+                    assert capi.afsai_bounded_stripes(me, rows, k) == oracle.stripes_used(H, me, k), (npr, k, me)
