@@ -113,6 +113,25 @@ def test_M3_full_size(ctx):
     F.close()
 
 
+def test_M3_full_size_fp32(ctx):
+    """The single-precision set-up at full size: seeded rows and every retried
+    row bitwise against the fp32 oracle; PCG iterations within 1.2x of the fp64 golden."""
+    from paper_2010_14175_b200.api import DeviceCSR, Factor
+    cfg = ai.CONFIGS["M3"]
+    A = cfg["make"]()
+    k, s, cap = cfg["nsteps"], cfg["s"], cfg["max_row_nnz"]
+    F = Factor(ctx, DeviceCSR.from_numpy(A), k, s, 0.0, cap, precision="fp32")
+    rp, ci, v = (t.cpu().numpy() for t in F.G())
+    rows = np.unique(np.concatenate([ai.sample_rows(A.n, 400, sub=11), F.retried_rows()])).astype(np.int64)
+    ref = oracle.setup(A, k, s, 0.0, cap, rows=rows, trace=False, precision="fp32")
+    bad = check_rows(rp, ci, v, ref, rows)
+    assert not bad, f"{len(bad)} of {len(rows)} rows differ: {bad[:10]}"
+    b, _ = ai.rhs_for(A)
+    x, rep = F.pcg(torch.from_numpy(b).cuda(), tol=1e-8, max_iters=20000)
+    assert rep["converged"] and rep["iters"] <= int(np.ceil(1.2 * golden("M3")["pcg_iters"]))
+    F.close()
+
+
 def test_M4_full_size(ctx):
     cfg = ai.CONFIGS["M4"]
     A = cfg["make"]()
