@@ -275,12 +275,6 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     a.lcap = lcap;
     bool first = true;
     DevBuf lu_buf;  // the pattern-row kernel's lu lists (global memory, one region per warp)
-#ifdef AFSAI_L_GLOBAL
-    const bool l_global = true;  // the lockstep kernel keeps L in global memory
-#else
-    const bool l_global = false;
-#endif
-    DevBuf L_buf;
     // One pass of the current plan over rows (device list) or [row_lo, row_lo+n);
     // returns the number of rows that overflowed an on-chip table in *rc.
     unsigned long long why = 0;  // overflow reasons of the last pass (lockstep kernel): 1 table, 2 slots, 4 hits
@@ -305,8 +299,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
         }
         if (!f) return set_status(status, AFSAI_ELIMIT, "no kernel instance for this pattern size");
-        const bool lg = l_global && hits && lockstep && f == lockstep_kernel_for(ls_lpr, mmax, p.s, hc);
-        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc, lg)
+        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc)
                            : prow ? prow_row_bytes(H, mmax, p.s, lcap)
                                   : scan_row_bytes(H, mmax, p.s);
         a.warp_smem = (int32_t)rb;
@@ -335,13 +328,6 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         occ = std::max(1, occ);
         int64_t grid = (int64_t)ctx->num_sms * occ;
         grid = std::max<int64_t>(1, std::min<int64_t>(grid, (n + rows_per_cta - 1) / rows_per_cta));
-        if (lg) {
-            // per-row L regions (+32 reals: the back-substitution's dead over-reads)
-            a.L_stride = ((int64_t)mmax * (mmax + 1)) / 2 + 1 + 32;
-            const size_t need = (size_t)grid * rows_per_cta * (size_t)a.L_stride * (f32 ? 4 : 8);
-            if (L_buf.bytes < need) AFSAI_CUDA_TRY(L_buf.alloc(need, ctx->stream));
-            a.L_global = L_buf.p;
-        }
         if (f == prow_kernel_for(mmax, p.s, max_row_len)) {  // per-warp lu lists in global memory
             const size_t need = (size_t)grid * rows_per_cta * (size_t)lcap * sizeof(int16_t);
             if (lu_buf.bytes < need) AFSAI_CUDA_TRY(lu_buf.alloc(need, ctx->stream));
@@ -402,7 +388,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             if (why & 1) nH = 2 * H;
             if (why & 2) nC = std::min(kMaxCact, cact + std::max(8, cact / 2));
             if (nH == H && nC == cact) break;  // hit lists full: the retries take those rows
-            if (hits_row_bytes(nH, mmax, p.s, nC, hc, l_global && lockstep) * 2 > 200 * 1024) break;
+            if (hits_row_bytes(nH, mmax, p.s, nC, hc) * 2 > 200 * 1024) break;
             H = nH;
             cact = nC;
         }
@@ -434,7 +420,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             if (prow && prow_row_bytes(2 * H, mmax, p.s, lcap) <= 200 * 1024) {
                 H *= 2;  // pattern-row kernel with a larger table
             } else if (hits && lockstep && 2 * cact <= kMaxCact &&
-                       hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc, l_global && lockstep) * 2 <= 200 * 1024) {
+                       hits_row_bytes(2 * H, mmax, p.s, 2 * cact, hc) * 2 <= 200 * 1024) {
                 H *= 2;  // hit-list kernel with a larger table and more candidate slots
                 cact *= 2;
             } else {

@@ -393,10 +393,9 @@ SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc) {
     return hc <= 6 ? hits_nt<32, 6>(nt, gs) : hits_nt<32, 8>(nt, gs);
 }
 
-int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc, bool l_global) {
+int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc) {
     const int gs = s < kMaxGroup ? s : kMaxGroup;
-    return hc <= 6 ? hit_state_bytes<6>(H, mmax, s, cact, s > gs, l_global)
-                   : hit_state_bytes<8>(H, mmax, s, cact, s > gs, l_global);
+    return hc <= 6 ? hit_state_bytes<6>(H, mmax, s, cact, s > gs) : hit_state_bytes<8>(H, mmax, s, cact, s > gs);
 }
 }  // namespace AFSAI_PNS
 }  // namespace afsai

@@ -17,7 +17,6 @@ typedef int8_t hit_t;
 
 struct HitState {
     real *inv, *y, *g, *L, *arow, *brow, *dscr, *acc;
-    real *bc;  // L in global memory: broadcast slots [2][S] (stage parity)
     hit_t *hv;
     int64_t *gstart;
     int32_t *hkey, *P, *sel, *sela, *glen, *misc, *akey, *prs;
@@ -27,11 +26,8 @@ struct HitState {
 };
 
 template <int HC>
-__host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc, bool l_global = false) {
-    // l_global: L lives in global memory (lockstep kernel, AFSAI_L_GLOBAL); 2 S reals of
-    // broadcast slots stay in shared memory
-    const int64_t lsz = l_global ? 2 * (int64_t)S : (M * (M + 1)) / 2 + 1;
-    int64_t dbl = 3 * (int64_t)M + lsz + (int64_t)S * M + S + 2 + (acc ? CA : 0);
+__host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc) {
+    int64_t dbl = 3 * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (acc ? CA : 0);
     int64_t i64 = S;
     int64_t i32 = (int64_t)H + M + 3 * S + 8 + (int64_t)CA + M;  // ... akey, prs
     int64_t i16 = 2 * (int64_t)CA;
@@ -41,7 +37,7 @@ __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, 
 }
 
 template <int HC>
-__device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, bool acc, real *Lg = nullptr) {
+__device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, bool acc) {
     HitState w;
     const int H = a.H, M = a.mmax, S = a.s, CA = a.cact;
     w.M = M;
@@ -52,13 +48,7 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     w.g = d; d += M;
     w.inv = d; d += M;
     w.y = d; d += M;
-    if (Lg) {
-        w.L = Lg;
-        w.bc = d; d += 2 * S;
-    } else {
-        w.L = d; d += (M * (M + 1)) / 2 + 1;
-        w.bc = nullptr;
-    }
+    w.L = d; d += (M * (M + 1)) / 2 + 1;
     w.arow = d; d += S * M;
     w.brow = d; d += S;
     w.dscr = d; d += 2;

@@ -24,8 +24,6 @@ struct SetupKArgs {
     int32_t cact;       // hit-list kernel: active candidate slots per row
     int32_t lcap;       // pattern-row kernel: list entries per row
     int16_t *lu_global; // pattern-row kernel: per-warp lu lists (lcap each) in global memory
-    void *L_global;     // lockstep kernel (AFSAI_L_GLOBAL): per-row L regions in global memory
-    int64_t L_stride;   //   reals per region
     int32_t warp_smem;  // bytes of shared memory per row (group)
     // outputs, index = global row - out_base
     int64_t out_base;
@@ -53,7 +51,7 @@ using SetupKernFn = void (*)(SetupKArgs);
     int64_t scan_row_bytes(int H, int mmax, int s);                                                    \
     /* hit-list kernel: rows of A with at most hc + 1 entries (stencils) */                          \
     SetupKernFn hits_kernel_for(int lpr, int mmax, int s, int hc);                                     \
-    int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc, bool l_global);                   \
+    int64_t hits_row_bytes(int H, int mmax, int s, int cact, int hc);                                  \
     /* hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4,                 \
        mmax <= 6*lpr) */                                                                               \
     SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);                                 \

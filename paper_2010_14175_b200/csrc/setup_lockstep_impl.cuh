@@ -210,27 +210,12 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
             real l[GS];
             // the owner stores L[q][k] (a predicated store, no divergence) and every
             // lane reads it back: a shared-memory broadcast instead of 64-bit shuffles
-#ifdef AFSAI_L_GLOBAL
-            // L in global memory: the broadcast goes through two shared slots per new
-            // row (stage parity), the owner also writes L[q][k] for later steps
-#pragma unroll
-            for (int u = 0; u < GS; ++u)
-                if (gl == ln && live && st[u]) {
-                    const real v = t[u][tt] * ivc[tt];
-                    w.bc[(k & 1) * GS + u] = v;
-                    Lnew[u][k] = v;
-                }
-            G.sync();
-#pragma unroll
-            for (int u = 0; u < GS; ++u) l[u] = w.bc[(k & 1) * GS + u];  // dead rows: any value
-#else
 #pragma unroll
             for (int u = 0; u < GS; ++u)
                 if (gl == ln && live && st[u]) Lnew[u][k] = t[u][tt] * ivc[tt];
             G.sync();
 #pragma unroll
             for (int u = 0; u < GS; ++u) l[u] = Lnew[u][k];  // dead rows: any value, folded into dead state
-#endif
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
@@ -339,14 +324,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
     const int lane = threadIdx.x & 31;
     const LGroup<LPR> G(lane);
     const int gl = G.gl;
-#ifdef AFSAI_L_GLOBAL
-    // L of this lane group's row in global memory (L1-resident while the row runs)
-    real *Lg = static_cast<real *>(a.L_global) +
-               (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR) * a.L_stride;
-#else
-    real *Lg = nullptr;
-#endif
-    HitState w = carve_hits<HC>(smem + (size_t)(threadIdx.x / LPR) * a.warp_smem, a, false, Lg);
+    HitState w = carve_hits<HC>(smem + (size_t)(threadIdx.x / LPR) * a.warp_smem, a, false);
     const int H = a.H, log2H = a.log2H, CA = w.CA;
     unsigned long long c_steps = 0, c_border = 0, c_back = 0, c_gfma = 0;
     unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
