@@ -359,6 +359,133 @@ void sort_gt_rows(int64_t n_rows, const int64_t *rowptr, int32_t *in_col, double
     *launches += 2;
 }
 
+// ---------------------------------------------------------------- transpose by stable radix sort
+// G^T as a stable LSD radix sort of G's entries by column (8-bit digits): the input
+// is G in row-major order, so every column's entries come out in ascending row --
+// the deterministic order C10 asks for, with no atomics and no per-row sort.
+// A pass = per-tile digit histograms, one exclusive scan (digit-major), a stable
+// scatter (ranks inside a tile from warp match masks and per-warp digit counts).
+constexpr int kRxThreads = 256, kRxItems = 16, kRxTile = kRxThreads * kRxItems;
+
+// keys (column - col_lo) and row ids of G's entries, in storage order
+__global__ void rx_init_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, int64_t col_lo,
+                               int64_t row_begin, int32_t *key, int32_t *row) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n_rows; r += nw)
+        for (int64_t e = rowptr[r] + lane; e < rowptr[r + 1]; e += 32) {
+            key[e] = (int32_t)(col[e] - col_lo);
+            row[e] = (int32_t)(r + row_begin);
+        }
+}
+
+__global__ void __launch_bounds__(kRxThreads) rx_hist_kernel(int64_t nnz, const int32_t *key, int shift,
+                                                             int64_t ntiles, int32_t *hist) {
+    __shared__ int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kRxTile;
+#pragma unroll 4
+    for (int k = 0; k < kRxItems; ++k) {
+        const int64_t e = t0 + k * kRxThreads + threadIdx.x;
+        if (e < nnz) atomicAdd(&h[(key[e] >> shift) & 255], 1);
+    }
+    __syncthreads();
+    hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter of one digit pass.  Items of a tile are taken in storage order
+// (iteration k: items t0 + 256 k + thread); an item's place in its digit bucket =
+// the bucket's start for this tile (scanned histogram) + items of the digit in
+// earlier iterations + in earlier warps of this iteration + earlier lanes of its warp.
+__global__ void __launch_bounds__(kRxThreads) rx_scatter_kernel(int64_t nnz, const int32_t *key,
+                                                                const int32_t *row, const double *val, int shift,
+                                                                int64_t ntiles, const int64_t *off, int32_t *okey,
+                                                                int32_t *orow, double *oval) {
+    constexpr int NW = kRxThreads / 32;
+    __shared__ int64_t base[256];
+    __shared__ int run[256];
+    __shared__ int wcnt[NW][256];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    base[tid] = off[(int64_t)tid * ntiles + blockIdx.x];
+    run[tid] = 0;
+    const int64_t t0 = (int64_t)blockIdx.x * kRxTile;
+    for (int k = 0; k < kRxItems; ++k) {
+#pragma unroll
+        for (int x = 0; x < NW; ++x) wcnt[x][tid] = 0;
+        __syncthreads();
+        const int64_t e = t0 + k * kRxThreads + tid;
+        const bool valid = e < nnz;
+        const int32_t kk = valid ? key[e] : 0;
+        const int d = valid ? (kk >> shift) & 255 : 256;  // 256: no digit
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && rank == 0) wcnt[w][d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            int pre = 0;
+            for (int x = 0; x < w; ++x) pre += wcnt[x][d];
+            const int64_t pos = base[d] + run[d] + pre + rank;
+            if (okey) okey[pos] = kk;
+            orow[pos] = row[e];
+            oval[pos] = val[e];
+        }
+        __syncthreads();
+        int add = 0;
+#pragma unroll
+        for (int x = 0; x < NW; ++x) add += wcnt[x][tid];
+        run[tid] += add;
+    }
+}
+
+int64_t radix_tmp_bytes(int64_t nnz, int64_t n_out) {
+    const int64_t ntiles = (nnz + kRxTile - 1) / kRxTile;
+    const int64_t nh = 256 * (ntiles > 0 ? ntiles : 1);
+    return nnz * (4 + 4 + 4 + 4 + 8 + 8) + nh * 4 + (nh + 1) * 8 + scan_tmp_elems(nh) * 8 + 64 * 6;
+}
+
+cudaError_t transpose_radix(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                            int64_t nnz, int64_t col_lo, int64_t n_out, int64_t row_begin, char *tmp,
+                            int32_t *t_col, double *t_val, int grid, cudaStream_t st, int64_t *launches) {
+    if (nnz == 0) return cudaSuccess;
+    const int64_t ntiles = (nnz + kRxTile - 1) / kRxTile;
+    const int64_t nh = 256 * ntiles;
+    auto carve = [&](size_t bytes) {
+        char *p = tmp;
+        tmp += (bytes + 63) & ~(size_t)63;
+        return p;
+    };
+    int32_t *key0 = (int32_t *)carve(nnz * 4), *row0 = (int32_t *)carve(nnz * 4);
+    int32_t *key1 = (int32_t *)carve(nnz * 4), *row1 = (int32_t *)carve(nnz * 4);
+    double *val0 = (double *)carve(nnz * 8), *val1 = (double *)carve(nnz * 8);
+    int32_t *hist = (int32_t *)carve(nh * 4);
+    int64_t *off = (int64_t *)carve((nh + 1) * 8);
+    int64_t *stiles = (int64_t *)carve(scan_tmp_elems(nh) * 8);
+    int bits = 1;
+    while (bits < 31 && (int64_t(1) << bits) < n_out) ++bits;
+    const int passes = (bits + 7) / 8;
+    rx_init_kernel<<<grid, 256, 0, st>>>(n_rows, rowptr, col, col_lo, row_begin, key0, row0);
+    *launches += 1;
+    const int32_t *ik = key0, *ir = row0;
+    const double *iv = val;
+    for (int ps = 0; ps < passes; ++ps) {
+        const bool last = ps == passes - 1;
+        int32_t *ok = last ? nullptr : (ps & 1 ? key0 : key1);
+        int32_t *orr = last ? t_col : (ps & 1 ? row0 : row1);
+        double *ov = last ? t_val : (ps & 1 ? val0 : val1);
+        rx_hist_kernel<<<(unsigned)ntiles, kRxThreads, 0, st>>>(nnz, ik, 8 * ps, ntiles, hist);
+        cudaError_t e = exclusive_scan(hist, nh, off, stiles, st, launches);
+        if (e != cudaSuccess) return e;
+        rx_scatter_kernel<<<(unsigned)ntiles, kRxThreads, 0, st>>>(nnz, ik, ir, iv, 8 * ps, ntiles, off, ok, orr, ov);
+        *launches += 2;
+        ik = ok;
+        ir = orr;
+        iv = ov;
+    }
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- multi-GPU helpers
 // lengths of local rows (int32) from a row pointer
 __global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len) {

@@ -24,6 +24,13 @@ __global__ void scatter_t_kernel(int64_t n_rows, const int64_t *rowptr, const in
 // sort every row of a scattered G^T by source row (C10); in_* is clobbered
 void sort_gt_rows(int64_t n_rows, const int64_t *rowptr, int32_t *in_col, double *in_val, int32_t *out_col,
                   double *out_val, int grid, cudaStream_t st, int64_t *launches);
+// G^T (columns [col_lo, col_lo + n_out) of G) by a stable LSD radix sort of G's entries by
+// column: writes t_col (source rows) and t_val in G^T's CSR order (t_rowptr from the
+// column counts).  tmp: radix_tmp_bytes(nnz, n_out) bytes of device scratch.
+int64_t radix_tmp_bytes(int64_t nnz, int64_t n_out);
+cudaError_t transpose_radix(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
+                            int64_t nnz, int64_t col_lo, int64_t n_out, int64_t row_begin, char *tmp,
+                            int32_t *t_col, double *t_val, int grid, cudaStream_t st, int64_t *launches);
 __global__ void row_lengths_kernel(const int64_t *rowptr, int64_t n_rows, int32_t *len);
 __global__ void g_triples_kernel(int64_t n_rows, const int64_t *rowptr, const int32_t *col, const double *val,
                                  int64_t row_begin, int32_t *tc, int32_t *tr, double *tv);

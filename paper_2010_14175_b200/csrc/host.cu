@@ -853,8 +853,21 @@ int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out
                                   &ctx->launches));
     F->nnz_Gt = nnz;  // one GPU: every entry lands locally
     if (F->t_col.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
-        F->t_val.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st) != cudaSuccess ||
-        tcol.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
+        F->t_val.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st) != cudaSuccess)
+        return set_status(status, AFSAI_ENOMEM, "G^T");
+    const char *tenv = std::getenv("AFSAI_TRANSPOSE");
+    if (!(tenv && std::strcmp(tenv, "atomic") == 0)) {
+        // stable radix sort by column (deterministic, no atomics, no per-row sort)
+        DevBuf rx;
+        if (rx.alloc((size_t)radix_tmp_bytes(nnz, n_out), st) != cudaSuccess)
+            return set_status(status, AFSAI_ENOMEM, "G^T radix scratch");
+        AFSAI_CUDA_TRY(transpose_radix(F->n_rows, F->g_rowptr.as<int64_t>(), F->g_col.as<int32_t>(),
+                                       F->g_val.as<double>(), nnz, col_lo, n_out, F->row_begin, rx.as<char>(),
+                                       F->t_col.as<int32_t>(), F->t_val.as<double>(), grid, st, &ctx->launches));
+        return AFSAI_OK;
+    }
+    // AFSAI_TRANSPOSE=atomic: scatter with column cursors, then a per-row sort (round 1)
+    if (tcol.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
         tval.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st) != cudaSuccess)
         return set_status(status, AFSAI_ENOMEM, "G^T");
     AFSAI_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, std::max<int64_t>(n_out, 1) * sizeof(int32_t), st));
