@@ -856,8 +856,9 @@ int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out
         F->t_val.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st) != cudaSuccess)
         return set_status(status, AFSAI_ENOMEM, "G^T");
     const char *tenv = std::getenv("AFSAI_TRANSPOSE");
-    if (!(tenv && std::strcmp(tenv, "atomic") == 0)) {
-        // stable radix sort by column (deterministic, no atomics, no per-row sort)
+    if (tenv && std::strcmp(tenv, "radix") == 0) {
+        // stable radix sort by column (no atomics, no per-row sort; 27.7 vs 24.2 ms on
+        // M3, so the atomic scatter + sort below stays the default)
         DevBuf rx;
         if (rx.alloc((size_t)radix_tmp_bytes(nnz, n_out), st) != cudaSuccess)
             return set_status(status, AFSAI_ENOMEM, "G^T radix scratch");
@@ -866,7 +867,7 @@ int transpose_G(afsai_ctx_t ctx, afsai_factor_t F, int64_t col_lo, int64_t n_out
                                        F->t_col.as<int32_t>(), F->t_val.as<double>(), grid, st, &ctx->launches));
         return AFSAI_OK;
     }
-    // AFSAI_TRANSPOSE=atomic: scatter with column cursors, then a per-row sort (round 1)
+    // scatter with column cursors (atomics), then a per-row sort into source-row order
     if (tcol.alloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), st) != cudaSuccess ||
         tval.alloc(std::max<int64_t>(nnz, 1) * sizeof(double), st) != cudaSuccess)
         return set_status(status, AFSAI_ENOMEM, "G^T");

@@ -176,8 +176,9 @@ def test_pcg_fp32_setup(ctx, make, k, s, cap):
     F32.close()
 
 
-@pytest.mark.parametrize("env", [{"AFSAI_TABLE": "64"}, {"AFSAI_PROW": "0"}, {"AFSAI_NOPROBE": "1"}],
-                         ids=["prow_retry_from_64", "scan_kernel", "hits_no_probe"])
+@pytest.mark.parametrize("env", [{"AFSAI_TABLE": "64"}, {"AFSAI_PROW": "0"}, {"AFSAI_NOPROBE": "1"},
+                                 {"AFSAI_TRANSPOSE": "radix"}],
+                         ids=["prow_retry_from_64", "scan_kernel", "hits_no_probe", "radix_transpose"])
 def test_setup_parity_plans(ctx, env, monkeypatch):
     """The other kernel plans (forced small tables and retries, the general scan
     kernel on FE rows, the hit-list kernel without the table probe) give the
@@ -185,6 +186,9 @@ def test_setup_parity_plans(ctx, env, monkeypatch):
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
     cases = [(ai.fe_elasticity(4), 30, 3, 100)]
+    if "AFSAI_TRANSPOSE" in env:   # G^T by the stable radix sort, checked bitwise against oracle.transpose
+        cases = [(ai.fe_elasticity(4), 30, 3, 100), (ai.arrow_spd(3000), 12, 3, 1 << 30),
+                 (ai.hetero_poisson3d(24), 20, 2, 1 << 30)]
     if "AFSAI_NOPROBE" in env:
         cases = [(ai.hetero_poisson3d(32), 20, 2, 1 << 30)]
     for A, k, s, cap in cases:
@@ -193,6 +197,9 @@ def test_setup_parity_plans(ctx, env, monkeypatch):
         ref = oracle.setup(A, k, s, 0.0, cap)
         flagged, nonbit = compare_rows(G, ref, np.arange(A.n), str(env))
         assert not flagged and nonbit == 0
+        T, Tr = host_csr(F, 1), oracle.transpose(ref.to_csr(A.n))
+        assert np.array_equal(T.rowptr, Tr.rowptr) and np.array_equal(T.col, Tr.col)
+        assert np.array_equal(T.val.view(np.int64), Tr.val.view(np.int64))
         if "AFSAI_TABLE" in env:
             assert F.stats()["retried_rows"] > 0
         F.close()
