@@ -127,6 +127,28 @@ __device__ __forceinline__ bool better(float aa, int32_t ja, float ab, int32_t j
     return (ia > ib) || (ia == ib && ja < jb);
 }
 
+// Insert (ca, cj, ct) into the sorted top-GS list (ba, bj, bt) under better(),
+// dropping the last entry.  All GS comparisons are against the list as it was
+// (the list is sorted, so the outcomes are monotone in q) and the new list is
+// selected from them: two dependent steps per candidate instead of a GS-long
+// compare-and-swap chain, with the same result as the sequential insertion.
+template <int GS>
+__device__ __forceinline__ void topk_insert(real (&ba)[GS], int32_t (&bj)[GS], int32_t (&bt)[GS], real ca, int32_t cj,
+                                            int32_t ct) {
+    bool b[GS];
+#pragma unroll
+    for (int q = 0; q < GS; ++q) b[q] = better(ca, cj, ba[q], bj[q]);
+#pragma unroll
+    for (int q = GS - 1; q >= 1; --q) {
+        ba[q] = b[q] ? (b[q - 1] ? ba[q - 1] : ca) : ba[q];
+        bj[q] = b[q] ? (b[q - 1] ? bj[q - 1] : cj) : bj[q];
+        bt[q] = b[q] ? (b[q - 1] ? bt[q - 1] : ct) : bt[q];
+    }
+    ba[0] = b[0] ? ca : ba[0];
+    bj[0] = b[0] ? cj : bj[0];
+    bt[0] = b[0] ? ct : bt[0];
+}
+
 __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {
 #ifdef AFSAI_BOUNDS_CHECK
     if (r < a.a_lo || r > a.a_hi) {
@@ -160,7 +182,9 @@ __device__ __forceinline__ int64_t rp_of(const SetupKArgs &a, int64_t r) {
 // One copy of the stage per column chunk, not unrolled (the set-up kernels are
 // instruction-cache sensitive).  Every accumulator folds in k-ascending order,
 // exactly DESIGN.md C5.  Returns false on a pivot !(> 1e-30).
-template <int LPR, int NT, int GS, class State>
+//  kSmemBcast: the owner lane alone stores L[q][k] and every lane reads it back
+//  (shared-memory broadcast) instead of the 64-bit shuffles.
+template <int LPR, int NT, int GS, bool kSmemBcast = false, class State>
 __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs, int ug, real &psi) {
     const int M = w.M, gl = G.gl;
     real t[GS][NT], dg[GS], ty[GS], cp[GS][GS], ivc[NT];
@@ -198,13 +222,23 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2) lsm[t2] = Lr[t2][k];
             real l[GS];
+            if constexpr (kSmemBcast) {
 #pragma unroll
-            for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
-            // broadcast values: every lane stores the same bits (no divergent branch
-            // before the next stage's shuffles)
+                for (int u = 0; u < GS; ++u)
+                    if (gl == ln && u < gs) Lnew[u][k] = t[u][tt] * ivc[tt];
+                G.sync();
+                // rows u >= gs read any in-bounds value into their dead state
 #pragma unroll
-            for (int u = 0; u < GS; ++u)
-                if (u < gs) Lnew[u][k] = l[u];
+                for (int u = 0; u < GS; ++u) l[u] = Lnew[u][k];
+            } else {
+#pragma unroll
+                for (int u = 0; u < GS; ++u) l[u] = G.bcast(t[u][tt] * ivc[tt], ln);
+                // broadcast values: every lane stores the same bits (no divergent
+                // branch before the next stage's shuffles)
+#pragma unroll
+                for (int u = 0; u < GS; ++u)
+                    if (u < gs) Lnew[u][k] = l[u];
+            }
 #pragma unroll
             for (int t2 = tt; t2 < NT; ++t2)
 #pragma unroll
@@ -264,7 +298,7 @@ __device__ bool border_group(const State &w, const Group<LPR> &G, int qf, int gs
 // (every state layout puts arow and more after L) and feed dead accumulators
 // (c >= k: final), so the fold is unpredicated.  The owner multiplies by its
 // column's inverse diagonal, held in a register.
-template <int LPR, int NT, class State>
+template <int LPR, int NT, bool kSmemBcast = false, class State>
 __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
     const int gl = G.gl;
     real tb[NT], ivc[NT];
@@ -286,8 +320,15 @@ __device__ void back_substitute(const State &w, const Group<LPR> &G, int m) {
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) lk[t2] = pk[LPR * t2];
             pk -= k;
-            const real gk = G.bcast(tb[tt] * ivc[tt], ln);
-            w.g[k] = gk;  // broadcast value, stored by every lane
+            real gk;
+            if constexpr (kSmemBcast) {
+                if (gl == ln) w.g[k] = tb[tt] * ivc[tt];  // owner stores, every lane reads
+                G.sync();
+                gk = w.g[k];
+            } else {
+                gk = G.bcast(tb[tt] * ivc[tt], ln);
+                w.g[k] = gk;  // broadcast value, stored by every lane
+            }
 #pragma unroll
             for (int t2 = 0; t2 <= tt; ++t2) tb[t2] = fma(-lk[t2], gk, tb[t2]);
         }

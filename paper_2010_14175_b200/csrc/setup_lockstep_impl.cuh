@@ -405,18 +405,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     nc += cand;
                     real ca = cand ? fabs(acc) : -real(1);
                     int32_t cj = cand ? w.akey[aa] : 0x7fffffff, ct = aa;
-#pragma unroll
-                    for (int q = 0; q < GS; ++q) {
-                        const bool b = better(ca, cj, ba[q], bj[q]);
-                        const real ta = ba[q];
-                        const int32_t tj = bj[q], t2 = bt[q];
-                        ba[q] = b ? ca : ba[q];
-                        bj[q] = b ? cj : bj[q];
-                        bt[q] = b ? ct : bt[q];
-                        ca = b ? ta : ca;
-                        cj = b ? tj : cj;
-                        ct = b ? t2 : ct;
-                    }
+                    topk_insert<GS>(ba, bj, bt, ca, cj, ct);
                 }
             }
             // row extents of the lane's local top-GS candidates, loaded now: they

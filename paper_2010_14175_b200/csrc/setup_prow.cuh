@@ -28,6 +28,7 @@ struct PRowState {
     int4 *pd;         // [M+1] row descriptors in ascending column order (prow_fetch)
     int64_t *rstart;  // [M] first entry of pattern row q, relative to A's base
     int64_t *rend;    // [S] end entry of the rows selected this step
+    int64_t *srs, *sre;  // [S] row extents of the winners, by selection round
     int32_t *hkey, *P, *sel, *selt, *misc, *lofs;  // lofs [M]
     int16_t *lu;      // [LC]: slot of each entry below column i of the pattern rows (global memory)
     int8_t *hval;
@@ -37,7 +38,7 @@ struct PRowState {
 __host__ __device__ inline int64_t prow_state_bytes(int H, int M, int S, int LC) {
     int64_t dbl = 3 * (int64_t)M + 1 + (int64_t)(M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + H + 1;
     int64_t i128 = M + 1;
-    int64_t i64 = M + S;
+    int64_t i64 = M + 3 * S;
     int64_t i32 = (int64_t)H + M + 2 * S + 4 + M;
     // the lu lists live in global memory (one region per warp, L1/L2-resident; their
     // loads ride with the prefetched values): 67 -> 52 KB per FE row, 4 rows per SM
@@ -65,6 +66,8 @@ __device__ __forceinline__ PRowState carve_prow(char *base, const SetupKArgs &a)
     int64_t *l8 = reinterpret_cast<int64_t *>(w.pd + M + 1);
     w.rstart = l8; l8 += M;
     w.rend = l8; l8 += S;
+    w.srs = l8; l8 += S;
+    w.sre = l8; l8 += S;
     int32_t *ip = reinterpret_cast<int32_t *>(l8);
     w.hkey = ip; ip += H;
     w.P = ip; ip += M;

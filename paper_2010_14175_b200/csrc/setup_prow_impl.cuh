@@ -9,13 +9,26 @@
 namespace afsai {
 namespace AFSAI_PNS {
 
-#ifndef AFSAI_PROW_DEPTH
-#define AFSAI_PROW_DEPTH 6
+#ifndef AFSAI_PROW_BATCH
+#define AFSAI_PROW_BATCH 10
 #endif
-// pattern rows prefetched ahead in the gradient: the value loads come from L2
-// (~600 cycles under load), a row's fold is one LDS -> DFMA -> STS chain
-constexpr int kProwDepth = AFSAI_PROW_DEPTH;
+// pattern rows fetched per batch in the gradient.  The value and slot loads come
+// from L2 (~1.5k cycles under load, two dies); every load in flight shares one
+// scoreboard, so the loads of a batch are issued together and waited on once
+// (a rolling prefetch, 6-12 rows deep, waited for its newest load at every row:
+// M4 2.04 s; batches of 10: 1.75 s; two alternating batches of 6: 2.01 s;
+// DESIGN.md §4.1).  Registers cap the batch (11 per row; 12 rows: 254).
+constexpr int kProwBatch = AFSAI_PROW_BATCH;
 constexpr int kProwGather = 8;  // entries per lane loaded per gather batch
+// L[q][k] broadcast through shared memory in the bordering sweep (owner store,
+// __syncwarp, every lane loads) instead of 64-bit shuffles: M4 border phase
+// 351 -> 325 ms.  (The same for g~[k] in the back-substitution: 154 -> 180 ms, so
+// that one keeps the shuffle.)
+#ifdef AFSAI_PROW_BCAST_SHFL
+constexpr bool kProwSmemBcast = false;
+#else
+constexpr bool kProwSmemBcast = true;
+#endif
 
 // Insert-if-absent of one key per lane (lanes with !valid idle).  The probe loop
 // is controlled by a warp vote and its body is structured, so the warp leaves it
@@ -80,6 +93,20 @@ __device__ __forceinline__ void prow_fetch(const PRowState &w, const real *vrow,
         f.s[v] = in ? (int)lb[x] : spare;
         f.v[v] = in ? __ldg(vb + x) : real(0);
     }
+}
+
+// fold one fetched pattern row into acc: lanes without an entry fold 0 into the
+// spare slot.  A lane's slots within one row are distinct columns: all loads,
+// then all fmas, then all stores (one LDS -> DFMA -> STS chain per row).
+template <int NV>
+__device__ __forceinline__ void prow_fold(const PRowState &w, const PRowFetch<NV> &f) {
+    real av[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) av[v] = w.acc[f.s[v]];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) av[v] = fma(f.v[v], f.gq, av[v]);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) w.acc[f.s[v]] = av[v];
 }
 
 template <int LPR, int NT, int GS, int NV>
@@ -157,6 +184,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
         bool fail = false, overflow = (w.misc[1] != 0) || w.misc[0] * 4 > H * 3;
         int fail_code = 0, fail_step = 0;
         int lused = w.pd[0].z >> 16;  // list entries in use (group-uniform)
+        int gsum = lused;             // gradient fmas per step: entries below i of P's rows and row i
         PHASE(0)
 
         for (int k = 1; k <= a.nsteps && !overflow; ++k) {
@@ -170,35 +198,29 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             for (int sl = gl; sl < H; sl += LPR) w.acc[sl] = real(0);
             G.sync();
             {
-                PRowFetch<NV> pf[kProwDepth];
-#pragma unroll
+                // batches of kProwBatch pattern rows: all their loads are issued
+                // together and waited on once (the load scoreboard is shared by
+                // every load in flight, so a rolling prefetch would wait for the
+                // newest load at every row)
                 const real *vrow = aval(a) + e0i;
                 const int spare = H;
+                for (int base = 0; base <= m; base += kProwBatch) {
+                    PRowFetch<NV> pf[kProwBatch];
 #pragma unroll
-                for (int d = 0; d < kProwDepth; ++d) prow_fetch<LPR, NV>(w, vrow, spare, d, m, gl, pf[d]);
-                for (int base = 0; base <= m; base += kProwDepth) {
+                    for (int d = 0; d < kProwBatch; ++d) prow_fetch<LPR, NV>(w, vrow, spare, base + d, m, gl, pf[d]);
 #pragma unroll
-                    for (int d = 0; d < kProwDepth; ++d) {
+                    for (int d = 0; d < kProwBatch; ++d) {
                         if (base + d <= m) {
-                            // branch-free: lanes without an entry fold 0 into the
-                            // spare slot H.  A lane's slots within one row are
-                            // distinct columns: all loads, then all fmas, then all
-                            // stores (one LDS -> DFMA -> STS chain per row).
-                            real av[NV];
-#pragma unroll
-                            for (int v = 0; v < NV; ++v) av[v] = w.acc[pf[d].s[v]];
-#pragma unroll
-                            for (int v = 0; v < NV; ++v) av[v] = fma(pf[d].v[v], pf[d].gq, av[v]);
-#pragma unroll
-                            for (int v = 0; v < NV; ++v) w.acc[pf[d].s[v]] = av[v];
+                            prow_fold<NV>(w, pf[d]);
                             G.sync();
-                            prow_fetch<LPR, NV>(w, vrow, spare, base + d + kProwDepth, m, gl, pf[d]);
                         }
                     }
                 }
             }
-            if (gl == 0)
-                for (int x = 0; x <= m; ++x) c_gfma += (unsigned long long)(w.pd[x].z >> 16);
+            c_gfma += (unsigned long long)gsum;
+#ifdef AFSAI_PROW_DIAG
+            PHASE(0)  // diagnostics build: the fold goes to slot 0, the candidate scan stays in slot 1
+#endif
             // candidates: keys not in P with acc != 0; per-lane top-GS lists
             int nc = 0;
             real ba[GS];
@@ -212,19 +234,16 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 nc += cand;
                 real ca = cand ? fabs(acc) : -real(1);
                 int32_t cj = cand ? key : INT_MAX, ct = sl;
-                // insertion into the sorted top-GS list with selects (no branches)
+                topk_insert<GS>(ba, bj, bt, ca, cj, ct);
+            }
+            // row extents of the lane's local top-GS candidates, loaded now: they
+            // arrive during the group argmax; the winners' are stored by their lanes
+            int64_t rs[GS], re[GS];
 #pragma unroll
-                for (int q = 0; q < GS; ++q) {
-                    const bool b = better(ca, cj, ba[q], bj[q]);
-                    const real ta = ba[q];
-                    const int32_t tj = bj[q], t2 = bt[q];
-                    ba[q] = b ? ca : ba[q];
-                    bj[q] = b ? cj : bj[q];
-                    bt[q] = b ? ct : bt[q];
-                    ca = b ? ta : ca;
-                    cj = b ? tj : cj;
-                    ct = b ? t2 : ct;
-                }
+            for (int q = 0; q < GS; ++q) {
+                const bool ok = bt[q] >= 0;
+                rs[q] = ok ? rp_of(a, bj[q]) : 0;
+                re[q] = ok ? rp_of(a, (int64_t)bj[q] + 1) : 0;
             }
             nc = G.sum(nc);
             PHASE(1)
@@ -245,12 +264,16 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 if (me) {
                     w.sel[u] = wj;
                     w.selt[u] = bt[0];
+                    w.srs[u] = rs[0];
+                    w.sre[u] = re[0];
                 }
 #pragma unroll
                 for (int q = 0; q + 1 < GS; ++q) {
                     ba[q] = me ? ba[q + 1] : ba[q];
                     bj[q] = me ? bj[q + 1] : bj[q];
                     bt[q] = me ? bt[q + 1] : bt[q];
+                    rs[q] = me ? rs[q + 1] : rs[q];
+                    re[q] = me ? re[q + 1] : re[q];
                 }
                 ba[GS - 1] = me ? -real(1) : ba[GS - 1];
                 bj[GS - 1] = me ? INT_MAX : bj[GS - 1];
@@ -266,7 +289,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 int rank = 0;
                 for (int u = 0; u < nsel; ++u) rank += (w.sel[u] < j);
                 const int q = m + rank;
-                const int64_t rs = rp_of(a, j), re = rp_of(a, (int64_t)j + 1);
+                const int64_t rs = w.srs[mine ? gl : 0], re = w.sre[mine ? gl : 0];
                 if (mine) {
                     w.P[q] = j;
                     w.hval[w.selt[gl]] = (int8_t)q;
@@ -386,6 +409,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 full = __any_sync(0xffffffffu, full);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) nlow[q] = q < nsel ? G.sum(nlow[q]) : 0;
+                gsum += nlow[0] + nlow[1] + nlow[2] + nlow[3];
                 if (gl == 0) {
                     w.misc[0] += nins;
                     if (full) w.misc[1] = 1;
@@ -406,7 +430,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             // ---- phase B: bordered Cholesky of the new rows (C5-C6)
             for (int ug = 0; ug < nsel && !fail; ug += GS) {
                 const int gs = (nsel - ug) < GS ? (nsel - ug) : GS;
-                if (!border_group<LPR, NT, GS>(w, G, m + ug, gs, ug, psi)) {
+                if (!border_group<LPR, NT, GS, kProwSmemBcast>(w, G, m + ug, gs, ug, psi)) {
                     fail = true;
                     fail_code = AFSAI_ENOTSPD;
                     fail_step = k;
@@ -480,7 +504,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
         PHASE(6)
     }
 #undef PHASE
-    const unsigned long long g1 = c_gfma;  // counted by lane 0
+    const unsigned long long g1 = c_gfma;  // group-uniform; added once by lane 0
     if (gl == 0) {
         atomicAdd(&a.counters[0], c_steps);
         atomicAdd(&a.counters[1], c_border);
