@@ -62,6 +62,11 @@ __device__ __forceinline__ bool grid_reduce_last(double mine, double *partials, 
     return false;
 }
 
+#ifndef AFSAI_SPMV_UNROLL
+#define AFSAI_SPMV_UNROLL 4
+#endif
+constexpr int kSpmvU = AFSAI_SPMV_UNROLL;
+
 // y[row] = sum_e val[e] * x[col[e] - x_off]; optional fused dot sum_row y[row]*w[row]
 template <int W, int MODE>
 __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
@@ -79,20 +84,20 @@ __global__ void __launch_bounds__(256) spmv_kernel(SpmvArgs a) {
         if (row < a.n) {
             const int64_t e1 = a.rowptr[row + 1];
             int64_t e = a.rowptr[row] + sub;
-            // four entries per lane in flight (column loads, then the x gathers),
+            // kSpmvU entries per lane in flight (column loads, then the x gathers),
             // folded in the same ascending order as the plain loop
-            for (; e + 3 * W < e1; e += 4 * W) {
-                int32_t c[4];
-                double v[4], xv[4];
+            for (; e + (kSpmvU - 1) * W < e1; e += kSpmvU * W) {
+                int32_t c[kSpmvU];
+                double v[kSpmvU], xv[kSpmvU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kSpmvU; ++u) {
                     c[u] = __ldg(a.col + e + u * W);
                     v[u] = __ldg(a.val + e + u * W);
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) xv[u] = __ldg(a.x + (c[u] - a.x_off));
+                for (int u = 0; u < kSpmvU; ++u) xv[u] = __ldg(a.x + (c[u] - a.x_off));
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc = fma(v[u], xv[u], acc);
+                for (int u = 0; u < kSpmvU; ++u) acc = fma(v[u], xv[u], acc);
             }
             for (; e < e1; e += W) acc = fma(__ldg(a.val + e), __ldg(a.x + (__ldg(a.col + e) - a.x_off)), acc);
         }
