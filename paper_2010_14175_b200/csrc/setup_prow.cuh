@@ -31,6 +31,7 @@ struct PRowState {
     int64_t *srs, *sre;  // [S] row extents of the winners, by selection round
     int32_t *hkey, *P, *sel, *selt, *misc, *lofs;  // lofs [M]
     int16_t *lu;      // [LC]: slot of each entry below column i of the pattern rows (global memory)
+    int16_t *ulist;   // [H]: the occupied table slots in insertion order (the universe)
     int8_t *hval;
     int M;
 };
@@ -42,7 +43,7 @@ __host__ __device__ inline int64_t prow_state_bytes(int H, int M, int S, int LC)
     int64_t i32 = (int64_t)H + M + 2 * S + 4 + M;
     // the lu lists live in global memory (one region per warp, L1/L2-resident; their
     // loads ride with the prefetched values): 67 -> 52 KB per FE row, 4 rows per SM
-    int64_t i16 = 0;
+    int64_t i16 = H;  // ulist
     (void)LC;
     int64_t i8 = H;
     int64_t b = real_bytes(dbl) + 8 /* int4 alignment */ + i128 * 16 + i64 * 8 + i32 * 4 + i16 * 2 + i8;
@@ -77,6 +78,7 @@ __device__ __forceinline__ PRowState carve_prow(char *base, const SetupKArgs &a)
     w.lofs = ip; ip += M;
     int16_t *sp = reinterpret_cast<int16_t *>(ip);
     w.lu = a.lu_global + (int64_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * a.lcap;
+    w.ulist = sp; sp += H;
     w.hval = reinterpret_cast<int8_t *>(sp);
     return w;
 }

@@ -63,6 +63,14 @@ __device__ __forceinline__ int hinsert_warp(int32_t *hkey, int H, int log2H, boo
     return res;
 }
 
+// append the slots this call inserted (ins) to ulist, in lane order; ucnt is
+// group-uniform
+__device__ __forceinline__ void ulist_append(const PRowState &w, int gl, bool ins, int sl, int &ucnt) {
+    const unsigned bal = __ballot_sync(0xffffffffu, ins);
+    if (ins) w.ulist[ucnt + __popc(bal & ((1u << gl) - 1u))] = (int16_t)sl;
+    ucnt += __popc(bal);
+}
+
 // registers of one prefetched pattern row: its entries x = gl + LPR*v below
 // column i (slot, value) and g~ of the row
 template <int NV>
@@ -152,8 +160,8 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             w.g[M] = real(1);   // g~_i
         }
         G.sync();
+        int ucnt = 0;  // occupied slots = length of ulist (group-uniform)
         {
-            int nins = 0;
             bool full = false;
             for (int64_t e0 = e0i; e0 < e1i; e0 += LPR) {  // warp-uniform trip count
                 const int64_t e = e0 + gl;
@@ -168,11 +176,11 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                 bool ins;
                 const int sl = hinsert_warp(w.hkey, H, log2H, c < i, c, &ins);
                 if (c < i && sl >= 0) w.lu[e - e0i] = (int16_t)sl;
-                nins += __popc(__ballot_sync(0xffffffffu, ins));
+                ulist_append(w, gl, ins, sl, ucnt);
                 full |= __any_sync(0xffffffffu, c < i && sl < 0);
             }
             if (gl == 0) {
-                w.misc[0] = nins;
+                w.misc[0] = ucnt;
                 w.misc[1] = full ? 1 : 0;
             }
         }
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             // ---- phase G: gradient (C3) over the pattern rows in ascending column
             //      order, then row i; every acc[slot] sees the fma sequence of the
             //      storage order of its own row (bitwise symmetry, C1)
-            for (int sl = gl; sl < H; sl += LPR) w.acc[sl] = real(0);
+            for (int x = gl; x < ucnt; x += LPR) w.acc[w.ulist[x]] = real(0);
             G.sync();
             {
                 // batches of kProwBatch pattern rows: all their loads are issued
@@ -227,10 +235,13 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
             int32_t bj[GS], bt[GS];
 #pragma unroll
             for (int q = 0; q < GS; ++q) { ba[q] = -real(1); bj[q] = INT_MAX; bt[q] = -1; }
-            for (int sl = gl; sl < H; sl += LPR) {  // H is a multiple of LPR: no tail
+            // over the occupied slots only (ulist: about half of the table)
+            for (int x0 = 0; x0 < ucnt; x0 += LPR) {
+                const bool in = x0 + gl < ucnt;
+                const int sl = in ? w.ulist[x0 + gl] : 0;
                 const int32_t key = w.hkey[sl];
                 const real acc = w.acc[sl];
-                const bool cand = key != kEmpty && w.hval[sl] == kCand && acc != real(0);
+                const bool cand = in && w.hval[sl] == kCand && acc != real(0);
                 nc += cand;
                 real ca = cand ? fabs(acc) : -real(1);
                 int32_t cj = cand ? key : INT_MAX, ct = sl;
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                         pre[u] = acc_;  // end of row u
                     }
                 }
-                int nins = 0, nlow[4] = {0, 0, 0, 0};
+                int nlow[4] = {0, 0, 0, 0};
                 bool full = false;
                 for (int t0 = 0; t0 < total; t0 += LPR * kProwGather) {
                     int32_t cc[kProwGather];
@@ -398,20 +409,19 @@ __global__ void __launch_bounds__(128) afsai_setup_rows_prow_kernel(SetupKArgs a
                         if (ok) w.lu[lo_u + oo[b]] = (int16_t)sl;
                         const int st = ok ? (int)w.hval[sl] : -1;
                         if (st >= 0 && st <= m + u) w.arow[u * M + st] = vv[b];
+                        ulist_append(w, gl, ins, sl, ucnt);
                         // lane-local counts, reduced once after the gather
-                        nins += ins;
                         full |= low && sl < 0;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) nlow[q] += (ok && u == q);
                     }
                 }
-                nins = G.sum(nins);
                 full = __any_sync(0xffffffffu, full);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) nlow[q] = q < nsel ? G.sum(nlow[q]) : 0;
                 gsum += nlow[0] + nlow[1] + nlow[2] + nlow[3];
                 if (gl == 0) {
-                    w.misc[0] += nins;
+                    w.misc[0] = ucnt;
                     if (full) w.misc[1] = 1;
                 }
                 // descriptors of the new rows at their sorted positions
