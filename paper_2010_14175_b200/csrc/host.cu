@@ -167,6 +167,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     auto hits_kernel_for = kp::hits_kernel_for;
     auto hits_row_bytes = kp::hits_row_bytes;
     auto lockstep_kernel_for = kp::lockstep_kernel_for;
+    auto lockstep_row_bytes = kp::lockstep_row_bytes;
     auto prow_kernel_for = kp::prow_kernel_for;
     auto prow_row_bytes = kp::prow_row_bytes;
 #else
@@ -175,6 +176,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     auto hits_kernel_for = f32 ? sp::hits_kernel_for : dp::hits_kernel_for;
     auto hits_row_bytes = f32 ? sp::hits_row_bytes : dp::hits_row_bytes;
     auto lockstep_kernel_for = f32 ? sp::lockstep_kernel_for : dp::lockstep_kernel_for;
+    auto lockstep_row_bytes = f32 ? sp::lockstep_row_bytes : dp::lockstep_row_bytes;
     auto prow_kernel_for = f32 ? sp::prow_kernel_for : dp::prow_kernel_for;
     auto prow_row_bytes = f32 ? sp::prow_row_bytes : dp::prow_row_bytes;
 #endif
@@ -286,9 +288,10 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
         a.rows = rows;
         a.nrows = n;
         SetupKernFn f = nullptr;
+        bool ls = false;
         if (hits && lockstep) {
             f = lockstep_kernel_for(ls_lpr, mmax, p.s, hc);
-            if (f) lpr = ls_lpr;
+            if (f) { lpr = ls_lpr; ls = true; }
         }
         if (!f && prow) {
             f = prow_kernel_for(mmax, p.s, max_row_len);
@@ -299,7 +302,8 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             f = hits ? hits_kernel_for(lpr, mmax, p.s, hc) : scan_kernel_for(lpr, mmax, p.s);
         }
         if (!f) return set_status(status, AFSAI_ELIMIT, "no kernel instance for this pattern size");
-        const int64_t rb = hits ? hits_row_bytes(H, mmax, p.s, cact, hc)
+        const int64_t rb = ls ? lockstep_row_bytes(H, mmax, p.s, cact, hc)
+                           : hits ? hits_row_bytes(H, mmax, p.s, cact, hc)
                            : prow ? prow_row_bytes(H, mmax, p.s, lcap)
                                   : scan_row_bytes(H, mmax, p.s);
         a.warp_smem = (int32_t)rb;

@@ -55,6 +55,7 @@ using SetupKernFn = void (*)(SetupKArgs);
     /* hit-list kernel, 32/lpr rows per warp in lockstep (rows <= lpr entries, s <= 4,                 \
        mmax <= 6*lpr) */                                                                               \
     SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc);                                 \
+    int64_t lockstep_row_bytes(int H, int mmax, int s, int cact, int hc);                              \
     /* pattern-row kernel (long rows, s <= 4, mmax <= 128, rows <= 128 entries): 32 lanes per row */   \
     SetupKernFn prow_kernel_for(int mmax, int s, int64_t max_row_len);                                 \
     int64_t prow_row_bytes(int H, int mmax, int s, int lcap);

@@ -23,5 +23,9 @@ SetupKernFn lockstep_kernel_for(int lpr, int mmax, int s, int hc) {
         default: return ls_instance<4>(lpr, nt, hc);
     }
 }
+
+int64_t lockstep_row_bytes(int H, int mmax, int s, int cact, int hc) {
+    return hc <= 6 ? hit_state_bytes<6>(H, mmax, s, cact, false, true) : hit_state_bytes<8>(H, mmax, s, cact, false, true);
+}
 }  // namespace AFSAI_PNS
 }  // namespace afsai

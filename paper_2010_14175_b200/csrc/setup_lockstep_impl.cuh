@@ -120,7 +120,6 @@ __device__ void scan_row_hits_ls(const HitState &w, const LGroup<LPR> &G, int H,
             w.hval[sl] = (int8_t)-1;  // the key must not decode as an active slot
         } else {
             w.hval[sl] = (int8_t)(-2 - aa);
-            w.akey[aa] = c;
             w.ahs[aa] = (int16_t)sl;
             w.ahn[aa] = 1;
             w.ahq[aa] = (int8_t)q;
@@ -193,7 +192,7 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
         const int c = gl + LPR * tt;
         const bool old = active && c < qf;
         Lr[tt] = old ? w.L + tri(c) : w.L;  // dead columns: any in-bounds row
-        ivc[tt] = old ? w.inv[c] : real(0);
+        ivc[tt] = old ? w.L[tri(c) + c] : real(0);  // 1/L[c][c] in the diagonal slot
     }
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
@@ -246,7 +245,7 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
             const real inv_k = real(1) / dq;
             const real y_k = ty[uf] * inv_k;
             psi = fma(-y_k, y_k, psi);     // C6
-            w.inv[k] = inv_k;  // redundant values: every lane stores the same bits
+            w.L[tri(k) + k] = inv_k;  // 1/L[k][k] (diagonal slot); every lane stores the same bits
             w.y[k] = y_k;
             real lu[GS];
 #pragma unroll
@@ -288,7 +287,7 @@ __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool
         const int c = gl + LPR * tt;
         const bool in = active && c < m;
         tb[tt] = in ? w.y[c] : real(0);
-        ivc[tt] = in ? w.inv[c] : real(0);
+        ivc[tt] = in ? w.L[tri(c) + c] : real(0);
     }
     const real *pk = w.L + tri(m_max > 0 ? m_max - 1 : 0) + gl;  // row k, this lane's first column
 #pragma unroll
@@ -324,7 +323,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
     const int lane = threadIdx.x & 31;
     const LGroup<LPR> G(lane);
     const int gl = G.gl;
-    HitState w = carve_hits<HC>(smem + (size_t)(threadIdx.x / LPR) * a.warp_smem, a, false);
+    HitState w = carve_hits<HC>(smem + (size_t)(threadIdx.x / LPR) * a.warp_smem, a, false, true);
     const int H = a.H, log2H = a.log2H, CA = w.CA;
     unsigned long long c_steps = 0, c_border = 0, c_back = 0, c_gfma = 0;
     unsigned long long c_r0 = 0, c_r1 = 0, c_r2 = 0, c_r3 = 0, c_univ = 0;
@@ -417,8 +416,8 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     c_gfma += n0 + n1;
                     const bool cand0 = acc0 != real(0), cand1 = acc1 != real(0);
                     nc += cand0 + cand1;
-                    topk_insert<GS>(ba, bj, bt, cand0 ? fabs(acc0) : -real(1), cand0 ? w.akey[aa] : 0x7fffffff, aa);
-                    topk_insert<GS>(ba, bj, bt, cand1 ? fabs(acc1) : -real(1), cand1 ? w.akey[ab] : 0x7fffffff, ab);
+                    topk_insert<GS>(ba, bj, bt, cand0 ? fabs(acc0) : -real(1), cand0 ? w.hkey[w.ahs[aa]] : 0x7fffffff, aa);
+                    topk_insert<GS>(ba, bj, bt, cand1 ? fabs(acc1) : -real(1), cand1 ? w.hkey[w.ahs[ab]] : 0x7fffffff, ab);
                 }
             }
             // row extents of the lane's local top-GS candidates, loaded now: they
