@@ -13,10 +13,11 @@
 //
 // Per row (one group of LPR lanes), in shared memory:
 //   hash table hkey[H] (column -> slot), hval[H] (kCand or pattern position),
-//   acc[H] indexed by slot, and for each pattern row (and row i) the slots of
-//   its entries below column i (lu, filled once when the row joins P), so the
-//   gradient needs no hash lookups; the values themselves are re-read from L2,
-//   prefetched D rows ahead in registers.
+//   acc[H] indexed by slot, ulist (the occupied slots, in insertion order), L;
+// in a per-warp region of global memory: for each pattern row (and row i) the
+//   slots of its entries below column i (lu, filled once when the row joins P),
+//   so the gradient needs no hash lookups; the values themselves are re-read from
+//   L2, fetched into registers in batches of pattern rows (setup_prow_impl.cuh).
 #pragma once
 #include "setup_common.cuh"
 
@@ -42,7 +43,7 @@ __host__ __device__ inline int64_t prow_state_bytes(int H, int M, int S, int LC)
     int64_t i64 = M + 3 * S;
     int64_t i32 = (int64_t)H + M + 2 * S + 4 + M;
     // the lu lists live in global memory (one region per warp, L1/L2-resident; their
-    // loads ride with the prefetched values): 67 -> 52 KB per FE row, 4 rows per SM
+    // loads ride with the batched value loads): 67 -> 52 KB per FE row, 4 rows per SM
     int64_t i16 = H;  // ulist
     (void)LC;
     int64_t i8 = H;

@@ -71,12 +71,12 @@ __device__ __forceinline__ void ulist_append(const PRowState &w, int gl, bool in
     ucnt += __popc(bal);
 }
 
-// registers of one prefetched pattern row: its entries x = gl + LPR*v below
+// registers of one fetched pattern row: its entries x = gl + LPR*v below
 // column i (slot, value) and g~ of the row
 template <int NV>
 struct PRowFetch {
     real v[NV];
-    int s[NV];  // acc slot (H: the spare slot); 32-bit to keep the prefetch depth in registers
+    int s[NV];  // acc slot (H: the spare slot)
     real gq;
 };
 
