@@ -230,6 +230,9 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
     int cact = 56;  // active candidate slots (7-point interior rows peak near 50)
     // the hit-list kernels encode active slot aa as int8 state -2 - aa
     constexpr int kMaxCact = 126;
+    // the probe's growth cap on the active candidate slots (A/B knob)
+    int cact_cap = kMaxCact;
+    if (const char *e = std::getenv("AFSAI_CACT_MAX")) cact_cap = std::max(8, std::min(kMaxCact, std::atoi(e)));
     // pattern-row kernel for long rows (FE): universe ~ (mmax+1) * len / 10 keys,
     // table at most 3/4 full; lists hold every pattern row (no overflow)
     // (its row descriptors hold entry offsets relative to row i as int32)
@@ -390,7 +393,7 @@ int run_rows(afsai_ctx_t ctx, const DeviceCsr &Aext, int64_t a_lo, int64_t a_hi,
             int nH = H, nC = cact;
             if (!(hits && lockstep) || why == 0) why = 3;
             if (why & 1) nH = 2 * H;
-            if (why & 2) nC = std::min(kMaxCact, cact + std::max(8, cact / 2));
+            if (why & 2) nC = std::min(cact_cap, cact + std::max(8, cact / 2));
             if (nH == H && nC == cact) break;  // hit lists full: the retries take those rows
             if (hits_row_bytes(nH, mmax, p.s, nC, hc) * 2 > 200 * 1024) break;
             H = nH;

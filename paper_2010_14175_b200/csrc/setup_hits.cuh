@@ -26,11 +26,14 @@ struct HitState {
 };
 
 // compact (the lockstep kernel): no inv[] (1/L[k][k] lives in L's unused diagonal
-// slot) and no akey[] (a candidate's column is hkey[ahs[a]]): M doubles and CA ints
-// less per row (M3: 11.9 -> 11.2 KB, 20 instead of 18 rows per SM)
+// slot), no akey[] (a candidate's column is hkey[ahs[a]]) and no arow[] (a new
+// row's gathered A[P, P_q] is written straight into its own, still empty, row q of
+// L, the diagonal a_qq into the diagonal slot): (2 + S) M doubles and CA ints less
+// per row
 template <int HC>
 __host__ __device__ inline int64_t hit_state_bytes(int H, int M, int S, int CA, bool acc, bool compact = false) {
-    int64_t dbl = (compact ? 2 : 3) * (int64_t)M + (M * (M + 1)) / 2 + 1 + (int64_t)S * M + S + 2 + (acc ? CA : 0);
+    int64_t dbl = (compact ? 2 : 3) * (int64_t)M + (M * (M + 1)) / 2 + 1 + (compact ? 0 : (int64_t)S * M) + S + 2 +
+                  (acc ? CA : 0);
     int64_t i64 = S;
     int64_t i32 = (int64_t)H + M + 3 * S + 8 + (compact ? 0 : (int64_t)CA) + M;  // ... akey, prs
     int64_t i16 = 2 * (int64_t)CA;
@@ -53,7 +56,8 @@ __device__ __forceinline__ HitState carve_hits(char *base, const SetupKArgs &a, 
     if (!compact) { w.inv = d; d += M; }
     w.y = d; d += M;
     w.L = d; d += (M * (M + 1)) / 2 + 1;
-    w.arow = d; d += S * M;
+    w.arow = nullptr;
+    if (!compact) { w.arow = d; d += S * M; }
     w.brow = d; d += S;
     w.dscr = d; d += 2;
     w.acc = nullptr;

@@ -147,7 +147,7 @@ __device__ __forceinline__ void fma_if(bool p, float a, float b, float &d) {
         : "f"(a), "f"(b), "r"((int)p));
 }
 
-// Bordered Cholesky of the new rows q = qf .. qf+gs-1 (arow slots ug..), forward
+// Bordered Cholesky of the new rows q = qf .. qf+gs-1 (gathered into their L rows), forward
 // solve and psi update, in lockstep: the old-column stages run to the warp maximum
 // qf_max; a row's updates happen only while live (active && k < qf).
 //  - right-looking column sweep: at stage k the owner lane of column k turns its
@@ -173,7 +173,7 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
     bool st[GS];
 #pragma unroll
     for (int u = 0; u < GS; ++u) {
-        const real *ar = w.arow + (ug + u) * M;
+        const real *ar = w.L + tri(qf + u < M ? qf + u : 0);  // the gathered row, in place (compact state)
         const bool ur = active && u < gs;
         st[u] = ur;
 #pragma unroll
@@ -276,7 +276,8 @@ __device__ bool border_group_ls(const HitState &w, const LGroup<LPR> &G, bool ac
 // maximum m_max): descending column sweep; lane c folds fma(-L[k][c], g[k], t_c) for
 // k = m-1 down to c+1.  Row k of L is read contiguously by the lanes (a running
 // pointer: tri(k-1) = tri(k) - k); reads past the row's live columns land inside the
-// row's shared-memory region (carve_hits: arow follows L) and feed dead
+// row's shared-memory region (carve_hits: brow, dscr and the integer arrays follow
+// L) and feed dead
 // accumulators; a row's folds are predicated on its live stages (k < m).
 template <int LPR, int NT>
 __device__ void back_substitute_ls(const HitState &w, const LGroup<LPR> &G, bool active, int m, int m_max) {
@@ -494,13 +495,13 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
 #pragma unroll
                 for (int v = 0; v < GS; ++v) rk[u] += (selj[v] < selj[u]);
             }
-            // what border reads: the whole of each new row's gather slot, by fixed
-            // per-lane column tiles (predicated stores, no row-dependent loop)
+            // what border reads: the new rows q = m .. m+nsel-1 of L (the gather
+            // writes A[P_q, P] there), zeroed by fixed per-lane column tiles
 #pragma unroll
             for (int u = 0; u < GS; ++u)
 #pragma unroll
                 for (int tt = 0; tt < NT; ++tt)
-                    if (gl + LPR * tt < w.M) w.arow[u * w.M + gl + LPR * tt] = real(0);
+                    if (u < nsel && gl + LPR * tt <= m + u) w.L[tri(m + u) + gl + LPR * tt] = real(0);
             if (gl < nsel) w.brow[gl] = real(0);
             G.sync();
             if (gl < nsel) {
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(LPR == 16 ? 96 : 256, LPR == 16 ? 4 : 1) afsai
                     if (ug + u < nsel_max) {  // winner u (selection order) is pattern position m + rk[u]
                         const int r = rk[u] < GS ? rk[u] : 0;
                         scan_row_hits_ls<LPR, HC>(w, G, H, log2H, i, pvld[u], pc[u], pv[u], pe[u], m + r,
-                                                  w.arow + r * w.M, w.brow + r, bk);
+                                                  w.L + tri(m + r), w.brow + r, bk);
                     }
             }
             PHASE(3)
