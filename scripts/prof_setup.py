@@ -1,5 +1,10 @@
 """Profile helper: one warm-up + one measured afsai_setup on a Poisson cube (or FE),
-prints stats / phase shares as JSON.  Used under ncu for the set-up kernel."""
+prints stats / phase shares as JSON.  Used under ncu for the set-up kernel.
+phase_fp64_frac: per phase with fp64 work, the counted algorithmic FMAs x 2 over
+(the phase's share of the in-kernel clock64 cycles x the rows-kernel time) over the
+fp64 peak (37.2 TF: 148 SM x 64 DFMA/clk x 2 x 1965 MHz) -- the share-of-time split
+is an approximation (phases of different warps overlap).
+usage: prof_setup.py [poisson|hetero|fe] [N] [reps]"""
 import json
 import os
 import sys
@@ -40,4 +45,9 @@ names = ["prologue", "gradient", "select", "gather", "border", "backsub", "outpu
 tot = sum(ph)
 out["phase_share"] = {n: round(v / tot, 4) for n, v in zip(names, ph)}
 out["phase_cycles_per_row"] = {n: v / A.n for n, v in zip(names, ph)}
+PEAK = 148 * 64 * 2 * 1.965e9
+fl = {"gradient": st["fma_grad"], "border": st["fma_border"], "backsub": st["fma_backsub"]}
+out["phase_fp64_frac"] = {n: round(2 * f / (out["phase_share"][n] * st["ms_rows"] * 1e-3) / PEAK, 5)
+                          for n, f in fl.items() if out["phase_share"][n] > 0}
+out["kernel_fp64_frac"] = round(2 * sum(fl.values()) / (st["ms_rows"] * 1e-3) / PEAK, 5)
 print(json.dumps(out, indent=1))
